@@ -1,0 +1,333 @@
+"""bench.py -- batched RNEA throughput on B200 (BASELINE.json metric).
+
+Default workload (N=1): config C3 -- 30-link random serial chain, 1M states per
+GPU, fp64, inverse dynamics through the C ABI (rd_inverse_dynamics_f64).
+A step is one pass of the whole hot path (one RNEA over the batch).  Under
+torchrun each rank evaluates its own 1M-state shard (weak scaling, no
+data-path collective); the timed region is bracketed by barrier +
+synchronize and the max over ranks is reported.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--dtype f64]
+    python bench.py --impl reference      # the CPU oracle arm (rank 0 only)
+
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "RNEA evals/s (n=30 links, 1M states) at 1/2/4/8 B200; % of FP64 roofline"
+UNIT = "evals/s"
+# Nominal FP64 CUDA-core peak from the guide's unit counts and clock:
+# 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz.
+PEAK_F64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+PEAK_F32_TFLOPS = 2 * PEAK_F64_TFLOPS
+L2_BYTES = 126 * 2 ** 20
+
+
+def lean_flops_id(n: int) -> int:
+    """SURVEY §8(d) algorithmic flop count of one RNEA (FMA = 2, sincos excluded)."""
+    return 379 * n - 96
+
+
+def lean_flops_fd(n: int) -> int:
+    return 928 * n - 599
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                self.reasons |= int(self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join()
+
+    def summary(self):
+        busy = [s for s in self.samples]
+        return {
+            "sm_mhz": float(statistics.median(busy)) if busy else None,
+            "sm_max_mhz": self.max_mhz,
+            "samples": len(busy),
+            "reasons": [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1],
+        }
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_baseline(robot, g, cfg, n, seconds=10.0):
+    """The oracle as it stands on all host cores, on a bounded sample of the workload."""
+    import oracle
+    cores = os.cpu_count() or 1
+    chunk = 4096 * cores // 8 if cores >= 8 else 4096
+    done, t_total, b0 = 0, 0.0, 0
+    oracle.rnea_batch(robot, g, *synth.states(cfg["seed"], n, 0, 64, cfg["ranges"]), nthreads=cores)
+    while t_total < seconds and done < 4_000_000:
+        q, qd, qdd = synth.states(cfg["seed"], n, b0, b0 + chunk, cfg["ranges"])
+        t0 = time.perf_counter()
+        oracle.rnea_batch(robot, g, q, qd, qdd, nthreads=cores)
+        t_total += time.perf_counter() - t0
+        done += chunk
+        b0 += chunk
+    return {"value": done / t_total, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {done} states of the {cfg['name']} workload (n={n}), oracle::rnea "
+                      f"(C++ -O2, dense 6x6 Eq. 1-2) on {cores} host threads, {t_total:.1f} s"}
+
+
+def load_traffic(cfg_name: str, dtype: str):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(f"{cfg_name}_{dtype}")
+    except Exception:
+        return None
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle, timed as it stands (rank 0 only)."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    cfg = dict(synth.CONFIGS[args.config], name=args.config)
+    n = cfg["n"]
+    robot = synth.robot_for(cfg)
+    g = cfg["gravity"]
+    cores = os.cpu_count() or 1
+    sample = args.ref_sample
+    q, qd, qdd = synth.states(cfg["seed"], n, 0, sample, cfg["ranges"])
+    for _ in range(args.warmup):
+        oracle.rnea_batch(robot, g, q, qd, qdd, nthreads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.rnea_batch(robot, g, q, qd, qdd, nthreads=cores)
+    dt = time.perf_counter() - t0
+    value = sample * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: n={n} random chain RNEA (bounded sample of {sample} states/step)",
+                   "n": n, "states_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{sample} states of {args.config} per step, oracle::rnea on {cores} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3", choices=list(synth.CONFIGS))
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--strategy", default="auto")
+    ap.add_argument("--batch", type=int, default=0, help="states per GPU (default: the config's)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=65536)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import paper_1609_04493_b200 as rd
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = dict(synth.CONFIGS[args.config], name=args.config)
+    n = cfg["n"]
+    fd = args.config == "C4"
+    per_gpu = args.batch or cfg["batch"]
+    if args.scaling == "strong":
+        total = per_gpu
+        per_gpu = (total + world - 1) // world
+    b0 = rank * per_gpu
+    b1 = b0 + per_gpu
+    robot = synth.robot_for(cfg)
+    g = cfg["gravity"]
+    dt = torch.float64 if args.dtype == "f64" else torch.float32
+    # inputs: a pure function of the GLOBAL state index (any shard regenerates its slice)
+    q, qd, qdd = synth.states(cfg["seed"], n, b0, b1, cfg["ranges"])
+    model = rd.Model.from_robot(robot, g)
+    model.set_strategy(args.strategy)
+    tq, tqd, tqdd = (torch.from_numpy(x).to("cuda", dt) for x in (q, qd, qdd))
+    out = torch.empty_like(tq)
+    if fd:
+        tau_in = rd.inverse_dynamics(model, tq, tqd, tqdd)     # consistent torques (untimed)
+        step = lambda: rd.forward_dynamics(model, tq, tqd, tau_in, out)  # noqa: E731
+    else:
+        step = lambda: rd.inverse_dynamics(model, tq, tqd, tqdd, out)  # noqa: E731
+    in_bytes = 3 * n * per_gpu * tq.element_size()
+    l2_note = (f"inputs {in_bytes / 2**20:.0f} MiB > L2 {L2_BYTES / 2**20:.0f} MiB, no flush"
+               if in_bytes > 2 * L2_BYTES else "L2 flushed between steps (write of 2x L2)")
+    flush_buf = None if in_bytes > 2 * L2_BYTES else torch.empty(2 * L2_BYTES // 4, dtype=torch.float32,
+                                                                   device="cuda")
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches = 0
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clock = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    with clock:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for k in range(args.steps):
+            if flush_buf is not None:
+                flush_buf.zero_()
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+            launches += rd.last_launch_count()
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    kernel_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = t_start.elapsed_time(t_end) if flush_buf is None else sum(kernel_ms)
+    avg_kernel_ms = float(np.mean(kernel_ms))
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([total_ms, avg_kernel_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms, avg_kernel_ms = float(tt[0]), float(tt[1])
+    units = per_gpu * world * args.steps
+    value = units / (total_ms / 1e3)
+
+    # e2e: through the public host-buffer API (pinned host arrays, H2D + kernel + D2H per step)
+    e2e = None
+    if not fd and args.dtype == "f64" and args.e2e_steps > 0:
+        pq, pqd, pqdd = (torch.from_numpy(x).pin_memory() for x in (q, qd, qdd))
+        pout = torch.empty_like(pq).pin_memory()
+        rd.inverse_dynamics_host(model, pq, pqd, pqdd, pout)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            rd.inverse_dynamics_host(model, pq, pqd, pqdd, pout)
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            import torch.distributed as dist
+            tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt[0])
+        e2e = {"value": per_gpu * world * args.e2e_steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": 3 * n * per_gpu * 8 * world, "d2h_bytes_per_step": n * per_gpu * 8 * world,
+               "api": "rd_inverse_dynamics_host_f64 (pinned host buffers, chunked 2-stream pipeline)"}
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    flops = (lean_flops_fd(n) if fd else lean_flops_id(n)) * per_gpu
+    achieved = flops / (avg_kernel_ms / 1e3) / 1e12
+    peak = PEAK_F64_TFLOPS if args.dtype == "f64" else PEAK_F32_TFLOPS
+    traffic = load_traffic(args.config, args.dtype)
+    strat = model.resolve_strategy(per_gpu, args.dtype == "f64") if not fd else "aba_thread"
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak" if args.scaling == "weak" else "strong", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {'FD (ABA)' if fd else 'RNEA'} n={n} random serial chain, "
+                               f"{per_gpu} states per GPU" if cfg['robot'] == 'random' else
+                               f"{args.config}: {cfg['robot']} n={n}, {per_gpu} states per GPU",
+                   "n": n, "states_per_gpu": per_gpu, "global_batch": per_gpu * world,
+                   "parallelism": f"batch-sharded x{world} (no collective on the hot path)",
+                   "strategy": strat, "robot_seed": 1000 + n if cfg["robot"] == "random" else cfg["robot"],
+                   "state_seed": cfg["seed"], "l2": l2_note},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "flops_per_eval": lean_flops_fd(n) if fd else lean_flops_id(n),
+                     "peak_basis": "148 SM x 64 DFMA/clk x 2 x 1.965 GHz (guide unit counts; measured DFMA "
+                                   "microbench 34.0 TF/s, profiles/r01/peaks_alu.jsonl)"
+                                   + ("; fp32 = 2x" if args.dtype == "f32" else ""),
+                     "kernel_ms": avg_kernel_ms,
+                     "hbm_gbs": 32 * n * per_gpu / (avg_kernel_ms / 1e3) / 1e9 * (0.5 if args.dtype == "f32" else 1)},
+        "clocks": clock.summary(),
+        "gpu_launches": launches,
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(robot, g, cfg, n, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,137 @@
+/*
+ * rd.h -- C ABI of librd.so: batched rigid-body dynamics of an n-link serial
+ * chain on NVIDIA B200 (sm_100a), after arXiv 1609.04493 (PAPER.md, cited P:n).
+ *
+ * The library evaluates, for B independent states,
+ *   inverse dynamics  tau  = ID(q, qd, qdd, V_0, Vdot_0, F_{n+1})   Eq. (3)
+ *                     by the RNEA forward/backward recursions of Eq. (1)-(2)
+ *                     (P:60-78), i.e. the two scans of Alg. 1;
+ *   forward dynamics  qdd  = FD(q, qd, tau, V_0, Vdot_0, F_{n+1})   Eq. (4)
+ *                     by the articulated-body algorithm, Eq. (7)-(8)
+ *                     and Alg. 3, or by JSIIA, Eq. (6), (17), Alg. 2.
+ *
+ * Conventions (A1-A3): twists (v, w) linear first; wrenches (f, m);
+ * f_{i-1,i} = M_i exp([S_i] q_i) maps link-i coordinates to link-(i-1)
+ * coordinates; S_i and J_i are given in the link-i frame; gravity g
+ * enters as Vdot_0 = (-g, 0) (A3); V_0 = 0 and F_{n+1} = 0 unless set with
+ * rd_model_set_boundary.
+ *
+ * Memory: batch arrays are structure-of-arrays, link-major: x[i*batch + b] for
+ * link i (0-based) and state b; `lda` variants are not provided.  Device
+ * pointers must be 16-byte aligned device memory of the current CUDA device;
+ * outputs must not alias inputs.  The caller owns every I/O buffer; the model
+ * owns its constants and any workspace.
+ *
+ * Errors: every call returns rd_status_t; RD_OK == 0.  rd_last_error() returns
+ * a thread-local message for the last failing call on the calling thread.  No
+ * C++ exception crosses the ABI.  Kernel launches are asynchronous on `stream`
+ * (a cudaStream_t; NULL = legacy default stream) and the call returns after
+ * enqueue; a launch failure returns RD_E_CUDA.  batch == 0 is a no-op (RD_OK).
+ * Per-state numerical failure in FD (Omega_i = S_i^T Jhat_i S_i <= 0, A11)
+ * does not abort other states: that state's qdd is NaN.
+ */
+#ifndef RD_H_
+#define RD_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rd_model_s* rd_model_t;
+
+typedef enum {
+  RD_OK = 0,
+  RD_E_ARG = 1,          /* bad argument: n < 1, null/misaligned/aliased pointer, batch < 0 */
+  RD_E_MODEL = 2,        /* invalid model: non-unit twist, non-rigid M, non-SPD/non-rigid J */
+  RD_E_CUDA = 3,         /* CUDA error (no device, launch failure, ...) */
+  RD_E_NOMEM = 4,        /* device or host allocation failed */
+  RD_E_UNSUPPORTED = 5   /* valid request this build does not support */
+} rd_status_t;
+
+/* In-robot parallelisation strategy of the inverse-dynamics kernel (north_star (2)). */
+typedef enum {
+  RD_STRAT_AUTO = 0,      /* chosen per (n, dtype, batch) from the measured table */
+  RD_STRAT_THREAD = 1,    /* one thread per state, serial recursion (stash in TMEM/registers) */
+  RD_STRAT_WARP_SCAN = 2, /* one warp per state, lane = link, Kogge-Stone shuffle scans */
+  RD_STRAT_GENERIC = 3    /* one thread per state, any n, stash in a global workspace */
+} rd_strategy_t;
+
+/* Forward-dynamics algorithm. */
+typedef enum {
+  RD_FD_ABA = 0,          /* articulated-body algorithm, Eq. (7)-(8), Alg. 3 (default) */
+  RD_FD_JSIIA = 1         /* joint-space inertia inversion, Eq. (6)/(17), Alg. 2 (Cholesky) */
+} rd_fd_algo_t;
+
+/* Library version string. */
+const char* rd_version(void);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* rd_last_error(void);
+
+/* Create a model (P:25-36 nomenclature).  All arrays are HOST memory, row-major:
+ *   M[n][4][4]  home transform M_i = f_{i-1,i}(q_i = 0), frame i -> frame i-1;
+ *               rotation block orthonormal with det +1 (tol 1e-9), last row 0 0 0 1;
+ *   S[n][6]     joint twist S_i = (v, w) in the link-i frame: revolute/screw
+ *               |w| = 1, or prismatic w = 0 and |v| = 1 (tol 1e-9);
+ *   J[n][6][6]  spatial inertia J_i about the link-i origin, (v, w) ordering,
+ *               rigid-body structure [[m I, -m[c]], [m[c], I_o]], symmetric (tol
+ *               1e-9 relative), m > 0 and positive-definite rotational inertia about
+ *               the centre of mass (the 6x6 is then SPD);
+ *   gravity[3]  base-frame gravity, realised as Vdot_0 = (-g, 0) (A3).
+ * On RD_E_MODEL the message lists every violation with its 1-based link index.
+ * The model is immutable afterwards except through rd_model_set_*; it holds
+ * device copies of the constants on the device current at creation.
+ */
+rd_status_t rd_model_create(int32_t n, const double* M, const double* S, const double* J,
+                            const double gravity[3], rd_model_t* out);
+
+rd_status_t rd_model_destroy(rd_model_t m);
+
+/* Number of links n. */
+int32_t rd_model_n(rd_model_t m);
+
+/* Override the inverse-dynamics strategy (RD_STRAT_AUTO restores the table). */
+rd_status_t rd_model_set_strategy(rd_model_t m, rd_strategy_t s);
+
+/* Strategy the next rd_inverse_dynamics_* call on `batch` states will use. */
+rd_strategy_t rd_model_resolve_strategy(rd_model_t m, int64_t batch, int32_t fp64);
+
+/* Full boundary data of Eq. (3)/(4): base twist V_0, base acceleration
+ * Vdot_0 (replaces the gravity-derived value; pass NULL to keep it) and tip
+ * wrench F_{n+1} acting on link n, expressed in frame n (f_{n,n+1} = I, A5).
+ * Host arrays of 6 doubles, NULL = zero (Vdot_0: NULL = keep gravity). */
+rd_status_t rd_model_set_boundary(rd_model_t m, const double V0[6], const double Vdot0[6],
+                                  const double Ftip[6]);
+
+/* Inverse dynamics (Eq. 1-2) on DEVICE arrays [n][batch]; tau is written. */
+rd_status_t rd_inverse_dynamics_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                    const double* qdd, double* tau, void* stream);
+rd_status_t rd_inverse_dynamics_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,
+                                    const float* qdd, float* tau, void* stream);
+
+/* Forward dynamics (Eq. 4) on DEVICE arrays [n][batch]; qdd is written.
+ * Uses a per-model device workspace, so concurrent FD calls on ONE model must be
+ * serialised by the caller (one model per stream otherwise). */
+rd_status_t rd_forward_dynamics_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                    const double* tau, double* qdd, void* stream);
+rd_status_t rd_forward_dynamics_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,
+                                    const float* tau, float* qdd, void* stream);
+rd_status_t rd_model_set_fd_algo(rd_model_t m, rd_fd_algo_t algo);
+
+/* End-to-end inverse dynamics on HOST arrays [n][batch] (pageable or pinned):
+ * the library streams the batch through device buffers in chunks, overlapping
+ * host->device copies, the kernel and device->host copies on its own streams,
+ * and returns after tau is complete in host memory (synchronous). */
+rd_status_t rd_inverse_dynamics_host_f64(rd_model_t m, int64_t batch, const double* q,
+                                         const double* qd, const double* qdd, double* tau);
+
+/* Number of kernel launches the last rd_* compute call on this thread enqueued. */
+int32_t rd_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RD_H_ */

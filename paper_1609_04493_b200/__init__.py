@@ -1,0 +1,214 @@
+"""paper_1609_04493_b200 -- batched robot dynamics on B200 (arXiv 1609.04493).
+
+Thin Python binding of librd.so (include/rd.h): argument marshalling only.
+Every step of the dynamics runs in the library's sm_100a kernels; PyTorch is
+used for device memory and streams.  There is no CPU fallback: if librd.so is
+missing or no CUDA device is present, calls raise.
+
+    import paper_1609_04493_b200 as rd
+    model = rd.Model(M, S, J, gravity=(0, 0, -9.81))   # numpy arrays, see include/rd.h
+    tau = rd.inverse_dynamics(model, q, qd, qdd)        # torch CUDA tensors [n, B]
+    qdd = rd.forward_dynamics(model, q, qd, tau)
+
+Names follow the paper: ID(q, qd, qdd) = tau (Eq. 3), FD(q, qd, tau) = qdd (Eq. 4).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["Model", "inverse_dynamics", "forward_dynamics", "inverse_dynamics_host", "lib",
+           "RdError", "STRATEGIES", "last_launch_count", "LIB_PATH"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librd.so")
+
+STRATEGIES = {"auto": 0, "thread": 1, "warp_scan": 2, "generic": 3}
+_STRAT_NAMES = {v: k for k, v in STRATEGIES.items()}
+FD_ALGOS = {"aba": 0, "jsiia": 1}
+
+# Symbols declared in include/rd.h (checked by tests/test_capi.py).
+EXPORTS = [
+    "rd_version", "rd_last_error", "rd_model_create", "rd_model_destroy", "rd_model_n",
+    "rd_model_set_strategy", "rd_model_resolve_strategy", "rd_model_set_boundary",
+    "rd_inverse_dynamics_f64", "rd_inverse_dynamics_f32", "rd_forward_dynamics_f64",
+    "rd_forward_dynamics_f32", "rd_model_set_fd_algo", "rd_inverse_dynamics_host_f64",
+    "rd_last_launch_count",
+]
+
+
+class RdError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Load librd.so (raises if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RdError(f"librd.so not found at {LIB_PATH}: run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        dp = ctypes.POINTER(ctypes.c_double)
+        L.rd_version.restype = ctypes.c_char_p
+        L.rd_last_error.restype = ctypes.c_char_p
+        L.rd_model_create.argtypes = [i32, dp, dp, dp, dp, ctypes.POINTER(vp)]
+        L.rd_model_destroy.argtypes = [vp]
+        L.rd_model_n.argtypes = [vp]
+        L.rd_model_n.restype = i32
+        L.rd_model_set_strategy.argtypes = [vp, ctypes.c_int]
+        L.rd_model_resolve_strategy.argtypes = [vp, i64, i32]
+        L.rd_model_resolve_strategy.restype = ctypes.c_int
+        L.rd_model_set_boundary.argtypes = [vp, dp, dp, dp]
+        L.rd_model_set_fd_algo.argtypes = [vp, ctypes.c_int]
+        for name in ("rd_inverse_dynamics_f64", "rd_inverse_dynamics_f32",
+                     "rd_forward_dynamics_f64", "rd_forward_dynamics_f32"):
+            getattr(L, name).argtypes = [vp, i64, vp, vp, vp, vp, vp]
+        L.rd_inverse_dynamics_host_f64.argtypes = [vp, i64, vp, vp, vp, vp]
+        L.rd_last_launch_count.restype = i32
+        for name in EXPORTS:
+            if name not in ("rd_version", "rd_last_error", "rd_model_n", "rd_model_resolve_strategy",
+                            "rd_last_launch_count"):
+                getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise RdError(f"{what}: status {rc}: {lib().rd_last_error().decode()}")
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def last_launch_count() -> int:
+    """Kernels the last rd_* compute call on this thread enqueued."""
+    return int(lib().rd_last_launch_count())
+
+
+class Model:
+    """A robot: M [n,4,4], S [n,6], J [n,6,6] (host float64), gravity (3,).
+
+    Created on the current CUDA device (rd_model_create, include/rd.h).
+    """
+
+    def __init__(self, M, S, J, gravity=(0.0, 0.0, -9.81)):
+        M, S, J = (np.ascontiguousarray(x, dtype=np.float64) for x in (M, S, J))
+        n = S.shape[0]
+        if M.shape != (n, 4, 4) or S.shape != (n, 6) or J.shape != (n, 6, 6):
+            raise ValueError("Model expects M [n,4,4], S [n,6], J [n,6,6]")
+        g = np.ascontiguousarray(gravity, dtype=np.float64).reshape(3)
+        h = ctypes.c_void_p()
+        _check(lib().rd_model_create(n, _dptr(M), _dptr(S), _dptr(J), _dptr(g), ctypes.byref(h)),
+               "rd_model_create")
+        self._h = h
+        self.n = n
+
+    @classmethod
+    def from_robot(cls, robot: dict, gravity=(0.0, 0.0, -9.81)):
+        return cls(robot["M"], robot["S"], robot["J"], gravity)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_strategy(self, name: str):
+        _check(lib().rd_model_set_strategy(self._h, STRATEGIES[name]), "rd_model_set_strategy")
+
+    def resolve_strategy(self, batch: int, fp64: bool = True) -> str:
+        return _STRAT_NAMES[lib().rd_model_resolve_strategy(self._h, int(batch), int(fp64))]
+
+    def set_fd_algo(self, name: str):
+        _check(lib().rd_model_set_fd_algo(self._h, FD_ALGOS[name]), "rd_model_set_fd_algo")
+
+    def set_boundary(self, V0=None, Vdot0=None, Ftip=None):
+        """Full Eq. (3) boundary: base twist, base acceleration, tip wrench (frame n)."""
+        arrs = [None if x is None else np.ascontiguousarray(x, dtype=np.float64).reshape(6)
+                for x in (V0, Vdot0, Ftip)]
+        ptrs = [None if a is None else _dptr(a) for a in arrs]
+        _check(lib().rd_model_set_boundary(self._h, *ptrs), "rd_model_set_boundary")
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().rd_model_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check_tensors(model: Model, *ts):
+    import torch
+    t0 = ts[0]
+    if not t0.is_cuda:
+        raise RdError("inputs must be CUDA tensors (use inverse_dynamics_host for host arrays)")
+    if t0.dtype not in (torch.float64, torch.float32):
+        raise RdError("dtype must be float64 or float32")
+    for t in ts:
+        if t.dtype != t0.dtype or t.device != t0.device or t.dim() != 2 or t.shape[0] != model.n \
+                or t.shape[1] != t0.shape[1] or not t.is_contiguous():
+            raise RdError("tensors must be contiguous [n, B] with one dtype/device")
+    return t0.dtype
+
+
+def inverse_dynamics(model: Model, q, qd, qdd, out=None, stream=None):
+    """tau = ID(q, qd, qdd) (Eq. 1-3) for B states; torch CUDA tensors [n, B]."""
+    import torch
+    dt = _check_tensors(model, q, qd, qdd)
+    if out is None:
+        out = torch.empty_like(q)
+    _check_tensors(model, q, out)
+    f = lib().rd_inverse_dynamics_f64 if dt == torch.float64 else lib().rd_inverse_dynamics_f32
+    _check(f(model.handle, q.shape[1], q.data_ptr(), qd.data_ptr(), qdd.data_ptr(), out.data_ptr(),
+             _stream_ptr(stream)), "rd_inverse_dynamics")
+    return out
+
+
+def forward_dynamics(model: Model, q, qd, tau, out=None, stream=None):
+    """qdd = FD(q, qd, tau) (Eq. 4, ABA Eq. 7-8) for B states; torch CUDA tensors [n, B]."""
+    import torch
+    dt = _check_tensors(model, q, qd, tau)
+    if out is None:
+        out = torch.empty_like(q)
+    _check_tensors(model, q, out)
+    f = lib().rd_forward_dynamics_f64 if dt == torch.float64 else lib().rd_forward_dynamics_f32
+    _check(f(model.handle, q.shape[1], q.data_ptr(), qd.data_ptr(), tau.data_ptr(), out.data_ptr(),
+             _stream_ptr(stream)), "rd_forward_dynamics")
+    return out
+
+
+def inverse_dynamics_host(model: Model, q, qd, qdd, out=None):
+    """End-to-end ID on HOST float64 arrays [n, B] (numpy or CPU torch, pinned preferred).
+
+    The library pipelines H2D copies, kernels and D2H copies on its own streams
+    and returns when tau is in host memory (rd_inverse_dynamics_host_f64).
+    """
+    def ptr(x):
+        if isinstance(x, np.ndarray):
+            if x.dtype != np.float64 or not x.flags.c_contiguous:
+                raise RdError("host arrays must be C-contiguous float64")
+            return x.ctypes.data
+        if x.dtype.__str__() != "torch.float64" or x.is_cuda or not x.is_contiguous():
+            raise RdError("host tensors must be contiguous CPU float64")
+        return x.data_ptr()
+    B = q.shape[1]
+    if out is None:
+        out = np.empty_like(np.asarray(q)) if isinstance(q, np.ndarray) else q.new_empty(q.shape)
+    _check(lib().rd_inverse_dynamics_host_f64(model.handle, B, ptr(q), ptr(qd), ptr(qdd), ptr(out)),
+           "rd_inverse_dynamics_host_f64")
+    return out

@@ -1,0 +1,586 @@
+// capi.cu -- the C ABI of librd.so (include/rd.h): model validation, the
+// joint-frame re-parameterisation, strategy dispatch, and the host-buffer
+// (end-to-end) pipeline.  No torch types, no exceptions across the ABI.
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rd.h"
+#include "rd_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+rd_status_t fail(rd_status_t st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+rd_status_t cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return RD_E_CUDA;
+}
+
+// ------------------------------------------------------------ small host algebra
+typedef double Mat3[3][3];
+typedef double Mat6[6][6];
+
+void skew(const double* a, Mat3 K) {
+  K[0][0] = 0; K[0][1] = -a[2]; K[0][2] = a[1];
+  K[1][0] = a[2]; K[1][1] = 0; K[1][2] = -a[0];
+  K[2][0] = -a[1]; K[2][1] = a[0]; K[2][2] = 0;
+}
+
+// Rigid transform (R, p) as 4x4 row-major.
+struct Rigid { double R[3][3]; double p[3]; };
+
+Rigid rigid_from4(const double* M) {
+  Rigid g;
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) g.R[i][j] = M[4 * i + j];
+    g.p[i] = M[4 * i + 3];
+  }
+  return g;
+}
+Rigid rigid_mul(const Rigid& a, const Rigid& b) {
+  Rigid c;
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) {
+      double s = 0;
+      for (int k = 0; k < 3; ++k) s += a.R[i][k] * b.R[k][j];
+      c.R[i][j] = s;
+    }
+    double t = a.p[i];
+    for (int k = 0; k < 3; ++k) t += a.R[i][k] * b.p[k];
+    c.p[i] = t;
+  }
+  return c;
+}
+Rigid rigid_inv(const Rigid& a) {
+  Rigid c;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) c.R[i][j] = a.R[j][i];
+  for (int i = 0; i < 3; ++i) {
+    double t = 0;
+    for (int k = 0; k < 3; ++k) t -= a.R[k][i] * a.p[k];
+    c.p[i] = t;
+  }
+  return c;
+}
+Rigid rigid_identity() {
+  Rigid g;
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) g.R[i][j] = (i == j);
+    g.p[i] = 0;
+  }
+  return g;
+}
+// Ad_g for (v, w) twists: [[R, [p]R], [0, R]].
+void adjoint(const Rigid& g, Mat6 A) {
+  Mat3 P;
+  skew(g.p, P);
+  for (int i = 0; i < 6; ++i) for (int j = 0; j < 6; ++j) A[i][j] = 0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      A[i][j] = g.R[i][j];
+      A[3 + i][3 + j] = g.R[i][j];
+      double s = 0;
+      for (int k = 0; k < 3; ++k) s += P[i][k] * g.R[k][j];
+      A[i][3 + j] = s;
+    }
+}
+
+// Rotation whose third column is the unit vector a.
+void frame_with_z(const double* a, double R[3][3]) {
+  double e[3] = {0, 0, 0};
+  int k = 0;
+  for (int i = 1; i < 3; ++i)
+    if (std::fabs(a[i]) < std::fabs(a[k])) k = i;
+  e[k] = 1.0;
+  double d = e[0] * a[0] + e[1] * a[1] + e[2] * a[2];
+  double x[3] = {e[0] - d * a[0], e[1] - d * a[1], e[2] - d * a[2]};
+  double nx = std::sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+  for (int i = 0; i < 3; ++i) x[i] /= nx;
+  double y[3] = {a[1] * x[2] - a[2] * x[1], a[2] * x[0] - a[0] * x[2], a[0] * x[1] - a[1] * x[0]};
+  for (int i = 0; i < 3; ++i) { R[i][0] = x[i]; R[i][1] = y[i]; R[i][2] = a[i]; }
+}
+
+bool cholesky6(const Mat6 A) {
+  double L[6][6] = {};
+  for (int j = 0; j < 6; ++j) {
+    double d = A[j][j];
+    for (int k = 0; k < j; ++k) d -= L[j][k] * L[j][k];
+    if (!(d > 0)) return false;
+    L[j][j] = std::sqrt(d);
+    for (int i = j + 1; i < 6; ++i) {
+      double s = A[i][j];
+      for (int k = 0; k < j; ++k) s -= L[i][k] * L[j][k];
+      L[i][j] = s / L[j][j];
+    }
+  }
+  return true;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ the model
+struct rd_model_s {
+  int n = 0;
+  int device = 0;
+  bool all_revolute = false;       // every joint revolute with zero pitch
+  rd_strategy_t strategy = RD_STRAT_AUTO;
+  rd_fd_algo_t fd_algo = RD_FD_ABA;
+  std::vector<rd::LinkConst<double>> L64;
+  std::vector<rd::LinkConst<float>> L32;
+  std::vector<Rigid> T;            // joint frame of link i expressed in the user's link-i frame
+  double gravity[3] = {0, 0, 0};
+  double V0[6] = {0}, Vd0[6] = {0}, Ftip_user[6] = {0};
+  rd::Boundary<double> b64;
+  rd::Boundary<float> b32;
+  rd::LinkConst<double>* dL64 = nullptr;
+  rd::LinkConst<float>* dL32 = nullptr;
+  void* ws = nullptr;              // generic/FD workspace (device)
+  size_t ws_bytes = 0;
+  // host-buffer pipeline
+  void* hbuf[2] = {nullptr, nullptr};
+  size_t hbuf_bytes = 0;
+  int64_t hchunk = 0;
+  cudaStream_t hstream[2] = {nullptr, nullptr};
+  std::mutex mu;
+};
+
+namespace {
+
+void rebuild_boundary(rd_model_t m) {
+  // Base quantities are unchanged by the joint frames (T_0 = I); the tip wrench
+  // is expressed in link n's joint frame: F' = Ad_{T_n}^T F (power pairing).
+  Mat6 A;
+  adjoint(m->T[m->n - 1], A);
+  double Ft[6];
+  for (int j = 0; j < 6; ++j) {
+    double s = 0;
+    for (int i = 0; i < 6; ++i) s += A[i][j] * m->Ftip_user[i];
+    Ft[j] = s;
+  }
+  for (int k = 0; k < 6; ++k) {
+    m->b64.V0[k] = m->V0[k];
+    m->b64.Vd0[k] = m->Vd0[k];
+    m->b64.Ftip[k] = Ft[k];
+    m->b32.V0[k] = (float)m->V0[k];
+    m->b32.Vd0[k] = (float)m->Vd0[k];
+    m->b32.Ftip[k] = (float)Ft[k];
+  }
+}
+
+rd_status_t ensure_ws(rd_model_t m, size_t bytes) {
+  if (m->ws_bytes >= bytes) return RD_OK;
+  if (m->ws) cudaFree(m->ws);
+  m->ws = nullptr;
+  m->ws_bytes = 0;
+  cudaError_t e = cudaMalloc(&m->ws, bytes);
+  if (e != cudaSuccess) return fail(RD_E_NOMEM, std::string("workspace cudaMalloc: ") + cudaGetErrorString(e));
+  m->ws_bytes = bytes;
+  return RD_OK;
+}
+
+template <typename T>
+bool is_device_ptr(const T* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <typename T>
+rd_status_t check_io(rd_model_t m, int64_t batch, const T* a, const T* b, const T* c, const T* out, bool device) {
+  if (!m) return fail(RD_E_ARG, "null model");
+  if (batch < 0) return fail(RD_E_ARG, "batch < 0");
+  if (batch == 0) return RD_OK;
+  const T* ins[3] = {a, b, c};
+  const char* names[4] = {"q", "qd", "third input", "output"};
+  const T* all[4] = {a, b, c, out};
+  for (int k = 0; k < 4; ++k) {
+    if (!all[k]) return fail(RD_E_ARG, std::string("null pointer: ") + names[k]);
+    if (reinterpret_cast<uintptr_t>(all[k]) % sizeof(T) != 0) return fail(RD_E_ARG, std::string("misaligned pointer: ") + names[k]);
+    if (device && !is_device_ptr(all[k])) return fail(RD_E_ARG, std::string("not device memory: ") + names[k]);
+  }
+  const size_t bytes = (size_t)m->n * (size_t)batch * sizeof(T);
+  for (int k = 0; k < 3; ++k) {
+    const char* lo = reinterpret_cast<const char*>(ins[k]);
+    const char* olo = reinterpret_cast<const char*>(out);
+    if (olo < lo + bytes && lo < olo + bytes) return fail(RD_E_ARG, std::string("output aliases input ") + names[k]);
+  }
+  int dev = -1;
+  cudaGetDevice(&dev);
+  if (device && dev != m->device) return fail(RD_E_ARG, "current CUDA device differs from the model's device");
+  return RD_OK;
+}
+
+template <typename T> const rd::LinkConst<T>* host_consts(rd_model_t m);
+template <> const rd::LinkConst<double>* host_consts<double>(rd_model_t m) { return m->L64.data(); }
+template <> const rd::LinkConst<float>* host_consts<float>(rd_model_t m) { return m->L32.data(); }
+template <typename T> const rd::LinkConst<T>* dev_consts(rd_model_t m);
+template <> const rd::LinkConst<double>* dev_consts<double>(rd_model_t m) { return m->dL64; }
+template <> const rd::LinkConst<float>* dev_consts<float>(rd_model_t m) { return m->dL32; }
+template <typename T> const rd::Boundary<T>& bnd(rd_model_t m);
+template <> const rd::Boundary<double>& bnd<double>(rd_model_t m) { return m->b64; }
+template <> const rd::Boundary<float>& bnd<float>(rd_model_t m) { return m->b32; }
+
+rd_strategy_t resolve(rd_model_t m, int64_t batch, bool fp64) {
+  (void)batch;
+  if (m->strategy == RD_STRAT_GENERIC) return RD_STRAT_GENERIC;
+  const bool thread_ok = m->all_revolute && rd::thread_kernel_has_n(m->n, fp64);
+  if (m->strategy == RD_STRAT_THREAD) return thread_ok ? RD_STRAT_THREAD : RD_STRAT_GENERIC;
+  if (m->strategy == RD_STRAT_WARP_SCAN) return RD_STRAT_WARP_SCAN;
+  return thread_ok ? RD_STRAT_THREAD : RD_STRAT_GENERIC;
+}
+
+template <typename T>
+rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* qd, const T* qdd, T* tau,
+                             void* stream) {
+  g_launches = 0;
+  rd_status_t st = check_io<T>(m, batch, q, qd, qdd, tau, true);
+  if (st != RD_OK || batch == 0) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  rd_strategy_t strat = resolve(m, batch, sizeof(T) == 8);
+  cudaError_t e = cudaSuccess;
+  if (strat == RD_STRAT_THREAD) {
+    bool ok = false;
+    e = rd::launch_rnea_thread<T>(m->n, host_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok);
+    if (!ok) strat = RD_STRAT_GENERIC;
+  } else if (strat == RD_STRAT_WARP_SCAN) {
+    bool ok = false;
+    e = rd::launch_rnea_warp<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok);
+    if (!ok) return fail(RD_E_UNSUPPORTED, "warp-scan strategy supports n <= 32 only");
+  }
+  if (strat == RD_STRAT_GENERIC) {
+    std::lock_guard<std::mutex> lk(m->mu);
+    const int64_t slots = rd::generic_ws_slots(batch);
+    st = ensure_ws(m, (size_t)slots * m->n * rd::generic_ws_per_link() * sizeof(T));
+    if (st != RD_OK) return st;
+    e = rd::launch_rnea_generic<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau,
+                                   reinterpret_cast<T*>(m->ws), slots, s, &g_launches);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "inverse dynamics launch");
+  return RD_OK;
+}
+
+template <typename T>
+rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* qd, const T* tau, T* qdd,
+                             void* stream) {
+  g_launches = 0;
+  rd_status_t st = check_io<T>(m, batch, q, qd, tau, qdd, true);
+  if (st != RD_OK || batch == 0) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  std::lock_guard<std::mutex> lk(m->mu);
+  const int64_t slots = rd::generic_ws_slots(batch);
+  st = ensure_ws(m, (size_t)slots * m->n * rd::aba_ws_per_link() * sizeof(T));
+  if (st != RD_OK) return st;
+  cudaError_t e = rd::launch_aba<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
+                                    reinterpret_cast<T*>(m->ws), slots, s, &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "forward dynamics launch");
+  return RD_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* rd_version(void) { return "rd 0.1 (sm_100a; arXiv 1609.04493 batched scan-RNEA)"; }
+const char* rd_last_error(void) { return g_err.c_str(); }
+int32_t rd_last_launch_count(void) { return g_launches; }
+
+rd_status_t rd_model_create(int32_t n, const double* M, const double* S, const double* J,
+                            const double gravity[3], rd_model_t* out) {
+  if (!out) return fail(RD_E_ARG, "null output handle");
+  *out = nullptr;
+  if (n < 1) return fail(RD_E_ARG, "n < 1");
+  if (!M || !S || !J || !gravity) return fail(RD_E_ARG, "null model array");
+  std::string viol;
+  auto add = [&](int i, const std::string& s) {
+    char buf[64];
+    snprintf(buf, sizeof buf, "link %d: ", i + 1);
+    if (!viol.empty()) viol += "; ";
+    viol += buf + s;
+  };
+  for (int i = 0; i < n; ++i) {
+    const double* Mi = M + 16 * i;
+    const double* Si = S + 6 * i;
+    const double* Ji = J + 36 * i;
+    bool finite = true;
+    for (int k = 0; k < 16; ++k) finite &= std::isfinite(Mi[k]);
+    for (int k = 0; k < 6; ++k) finite &= std::isfinite(Si[k]);
+    for (int k = 0; k < 36; ++k) finite &= std::isfinite(Ji[k]);
+    if (!finite) { add(i, "non-finite entry"); continue; }
+    // M: rigid transform
+    double orth = 0;
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double s = 0;
+        for (int k = 0; k < 3; ++k) s += Mi[4 * k + a] * Mi[4 * k + b];
+        orth = std::max(orth, std::fabs(s - (a == b)));
+      }
+    double det = Mi[0] * (Mi[5] * Mi[10] - Mi[6] * Mi[9]) - Mi[1] * (Mi[4] * Mi[10] - Mi[6] * Mi[8]) +
+                 Mi[2] * (Mi[4] * Mi[9] - Mi[5] * Mi[8]);
+    if (orth > 1e-9) add(i, "home transform rotation not orthonormal (err " + std::to_string(orth) + ")");
+    if (det < 0) add(i, "home transform rotation has det < 0");
+    if (Mi[12] != 0 || Mi[13] != 0 || Mi[14] != 0 || Mi[15] != 1) add(i, "home transform last row is not 0 0 0 1");
+    // S: unit twist
+    double wn = std::sqrt(Si[3] * Si[3] + Si[4] * Si[4] + Si[5] * Si[5]);
+    double vn = std::sqrt(Si[0] * Si[0] + Si[1] * Si[1] + Si[2] * Si[2]);
+    if (wn > 1e-9) {
+      if (std::fabs(wn - 1) > 1e-9) add(i, "joint twist angular norm " + std::to_string(wn) + " (must be 1)");
+    } else if (std::fabs(vn - 1) > 1e-9) {
+      add(i, "prismatic joint twist linear norm " + std::to_string(vn) + " (must be 1)");
+    }
+    // J: symmetric rigid-body spatial inertia, SPD
+    double jmax = 0, asym = 0;
+    for (int a = 0; a < 36; ++a) jmax = std::max(jmax, std::fabs(Ji[a]));
+    for (int a = 0; a < 6; ++a)
+      for (int b = 0; b < 6; ++b) asym = std::max(asym, std::fabs(Ji[6 * a + b] - Ji[6 * b + a]));
+    if (asym > 1e-9 * std::max(1.0, jmax)) add(i, "inertia not symmetric");
+    double mass = Ji[0];
+    double blk = 0;
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) blk = std::max(blk, std::fabs(Ji[6 * a + b] - (a == b ? mass : 0.0)));
+    double skw = 0;
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) skw = std::max(skw, std::fabs(Ji[6 * (3 + a) + b] + Ji[6 * (3 + b) + a]));
+    if (!(mass > 0)) add(i, "mass not positive");
+    if (blk > 1e-9 * std::max(1.0, jmax)) add(i, "inertia upper-left block is not m*I (not a rigid body)");
+    if (skw > 1e-9 * std::max(1.0, jmax)) add(i, "inertia off-diagonal block is not skew (not a rigid body)");
+    Mat6 A;
+    for (int a = 0; a < 6; ++a) for (int b = 0; b < 6; ++b) A[a][b] = 0.5 * (Ji[6 * a + b] + Ji[6 * b + a]);
+    if (!cholesky6(A)) add(i, "inertia not positive definite");
+  }
+  if (!viol.empty()) return fail(RD_E_MODEL, viol);
+
+  rd_model_t m = new (std::nothrow) rd_model_s;
+  if (!m) return fail(RD_E_NOMEM, "host allocation");
+  m->n = n;
+  cudaGetDevice(&m->device);
+  m->T.resize(n);
+  m->L64.resize(n);
+  m->L32.resize(n);
+  m->all_revolute = true;
+  // Joint frames: T_i = (R_a, r) with R_a e_z = joint axis and r the point of
+  // the axis closest to the link origin; then S'_i = Ad_{T_i^-1} S_i =
+  // (beta e_z, alpha e_z), M'_i = T_{i-1}^-1 M_i T_i, J'_i = Ad_{T_i}^T J_i Ad_{T_i}.
+  for (int i = 0; i < n; ++i) {
+    const double* Si = S + 6 * i;
+    double w[3] = {Si[3], Si[4], Si[5]}, v[3] = {Si[0], Si[1], Si[2]};
+    double wn = std::sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+    Rigid Ti;
+    double alpha, beta;
+    if (wn > 1e-9) {
+      for (int k = 0; k < 3; ++k) w[k] /= wn;
+      frame_with_z(w, Ti.R);
+      Ti.p[0] = w[1] * v[2] - w[2] * v[1];
+      Ti.p[1] = w[2] * v[0] - w[0] * v[2];
+      Ti.p[2] = w[0] * v[1] - w[1] * v[0];
+      alpha = 1.0;
+      beta = w[0] * v[0] + w[1] * v[1] + w[2] * v[2];   // pitch
+      if (std::fabs(beta) < 1e-14) beta = 0.0;
+    } else {
+      double vv[3] = {v[0], v[1], v[2]};
+      double vn = std::sqrt(vv[0] * vv[0] + vv[1] * vv[1] + vv[2] * vv[2]);
+      for (int k = 0; k < 3; ++k) vv[k] /= vn;
+      frame_with_z(vv, Ti.R);
+      Ti.p[0] = Ti.p[1] = Ti.p[2] = 0;
+      alpha = 0.0;
+      beta = 1.0;
+    }
+    if (!(alpha == 1.0 && beta == 0.0)) m->all_revolute = false;
+    m->T[i] = Ti;
+    Rigid Tprev = (i == 0) ? rigid_identity() : m->T[i - 1];
+    Rigid Mp = rigid_mul(rigid_mul(rigid_inv(Tprev), rigid_from4(M + 16 * i)), Ti);
+    Mat6 A;
+    adjoint(Ti, A);
+    const double* Ji = J + 36 * i;
+    double Jp[6][6];
+    for (int a = 0; a < 6; ++a)
+      for (int b = 0; b < 6; ++b) {
+        double s = 0;
+        for (int k = 0; k < 6; ++k)
+          for (int l = 0; l < 6; ++l) s += A[k][a] * Ji[6 * k + l] * A[l][b];
+        Jp[a][b] = s;
+      }
+    rd::LinkConst<double>& C = m->L64[i];
+    for (int a = 0; a < 3; ++a) {
+      for (int b = 0; b < 3; ++b) C.Rm[3 * a + b] = Mp.R[a][b];
+      C.pm[a] = Mp.p[a];
+    }
+    C.m = (Jp[0][0] + Jp[1][1] + Jp[2][2]) / 3.0;
+    C.h[0] = 0.5 * (Jp[5][1] - Jp[4][2]);
+    C.h[1] = 0.5 * (Jp[3][2] - Jp[5][0]);
+    C.h[2] = 0.5 * (Jp[4][0] - Jp[3][1]);
+    C.I[0] = Jp[3][3];
+    C.I[1] = Jp[4][4];
+    C.I[2] = Jp[5][5];
+    C.I[3] = 0.5 * (Jp[3][4] + Jp[4][3]);
+    C.I[4] = 0.5 * (Jp[3][5] + Jp[5][3]);
+    C.I[5] = 0.5 * (Jp[4][5] + Jp[5][4]);
+    C.alpha = alpha;
+    C.beta = beta;
+    rd::LinkConst<float>& F = m->L32[i];
+    for (int k = 0; k < 9; ++k) F.Rm[k] = (float)C.Rm[k];
+    for (int k = 0; k < 3; ++k) { F.pm[k] = (float)C.pm[k]; F.h[k] = (float)C.h[k]; }
+    for (int k = 0; k < 6; ++k) F.I[k] = (float)C.I[k];
+    F.m = (float)C.m;
+    F.alpha = (float)C.alpha;
+    F.beta = (float)C.beta;
+  }
+  for (int k = 0; k < 3; ++k) {
+    m->gravity[k] = gravity[k];
+    m->Vd0[k] = -gravity[k];     // reading A3: Vdot_0 = (-g, 0)
+  }
+  rebuild_boundary(m);
+  cudaError_t e = cudaMalloc(&m->dL64, sizeof(rd::LinkConst<double>) * n);
+  if (e == cudaSuccess) e = cudaMalloc(&m->dL32, sizeof(rd::LinkConst<float>) * n);
+  if (e == cudaSuccess) e = cudaMemcpy(m->dL64, m->L64.data(), sizeof(rd::LinkConst<double>) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(m->dL32, m->L32.data(), sizeof(rd::LinkConst<float>) * n, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    rd_model_destroy(m);
+    return cuda_fail(e, "model upload");
+  }
+  *out = m;
+  return RD_OK;
+}
+
+rd_status_t rd_model_destroy(rd_model_t m) {
+  if (!m) return RD_OK;
+  if (m->dL64) cudaFree(m->dL64);
+  if (m->dL32) cudaFree(m->dL32);
+  if (m->ws) cudaFree(m->ws);
+  for (int k = 0; k < 2; ++k) {
+    if (m->hbuf[k]) cudaFree(m->hbuf[k]);
+    if (m->hstream[k]) cudaStreamDestroy(m->hstream[k]);
+  }
+  delete m;
+  return RD_OK;
+}
+
+int32_t rd_model_n(rd_model_t m) { return m ? m->n : -1; }
+
+rd_status_t rd_model_set_strategy(rd_model_t m, rd_strategy_t s) {
+  if (!m) return fail(RD_E_ARG, "null model");
+  if (s < RD_STRAT_AUTO || s > RD_STRAT_GENERIC) return fail(RD_E_ARG, "unknown strategy");
+  m->strategy = s;
+  return RD_OK;
+}
+
+rd_strategy_t rd_model_resolve_strategy(rd_model_t m, int64_t batch, int32_t fp64) {
+  return m ? resolve(m, batch, fp64 != 0) : RD_STRAT_AUTO;
+}
+
+rd_status_t rd_model_set_fd_algo(rd_model_t m, rd_fd_algo_t algo) {
+  if (!m) return fail(RD_E_ARG, "null model");
+  if (algo != RD_FD_ABA && algo != RD_FD_JSIIA) return fail(RD_E_ARG, "unknown FD algorithm");
+  m->fd_algo = algo;
+  return RD_OK;
+}
+
+rd_status_t rd_model_set_boundary(rd_model_t m, const double V0[6], const double Vdot0[6], const double Ftip[6]) {
+  if (!m) return fail(RD_E_ARG, "null model");
+  for (int k = 0; k < 6; ++k) {
+    m->V0[k] = V0 ? V0[k] : 0.0;
+    m->Ftip_user[k] = Ftip ? Ftip[k] : 0.0;
+    if (Vdot0) m->Vd0[k] = Vdot0[k];
+  }
+  if (!Vdot0) {
+    for (int k = 0; k < 3; ++k) { m->Vd0[k] = -m->gravity[k]; m->Vd0[3 + k] = 0; }
+  }
+  rebuild_boundary(m);
+  return RD_OK;
+}
+
+rd_status_t rd_inverse_dynamics_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                    const double* qdd, double* tau, void* stream) {
+  return inverse_dynamics<double>(m, batch, q, qd, qdd, tau, stream);
+}
+rd_status_t rd_inverse_dynamics_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,
+                                    const float* qdd, float* tau, void* stream) {
+  return inverse_dynamics<float>(m, batch, q, qd, qdd, tau, stream);
+}
+rd_status_t rd_forward_dynamics_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                    const double* tau, double* qdd, void* stream) {
+  return forward_dynamics<double>(m, batch, q, qd, tau, qdd, stream);
+}
+rd_status_t rd_forward_dynamics_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,
+                                    const float* tau, float* qdd, void* stream) {
+  return forward_dynamics<float>(m, batch, q, qd, tau, qdd, stream);
+}
+
+// Host-buffer pipeline: chunks of `hchunk` states; chunk k uses device buffer
+// set k%2 and stream k%2: H2D(q,qd,qdd) -> kernel -> D2H(tau).  Two streams
+// overlap chunk k+1's copies with chunk k's kernel (PCIe is full duplex).
+rd_status_t rd_inverse_dynamics_host_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                         const double* qdd, double* tau) {
+  g_launches = 0;
+  rd_status_t st = check_io<double>(m, batch, q, qd, qdd, tau, false);
+  if (st != RD_OK || batch == 0) return st;
+  int dev = -1;
+  cudaGetDevice(&dev);
+  if (dev != m->device) return fail(RD_E_ARG, "current CUDA device differs from the model's device");
+  std::lock_guard<std::mutex> lk(m->mu);
+  const int n = m->n;
+  const int64_t chunk = std::min<int64_t>(batch, std::max<int64_t>(4096, (int64_t)(64ll << 20) / (8ll * n)));
+  const size_t set_bytes = (size_t)4 * n * chunk * sizeof(double);
+  if (m->hbuf_bytes < set_bytes) {
+    for (int k = 0; k < 2; ++k) {
+      if (m->hbuf[k]) cudaFree(m->hbuf[k]);
+      m->hbuf[k] = nullptr;
+    }
+    m->hbuf_bytes = 0;
+    for (int k = 0; k < 2; ++k) {
+      cudaError_t e = cudaMalloc(&m->hbuf[k], set_bytes);
+      if (e != cudaSuccess) return fail(RD_E_NOMEM, "host-path device buffers");
+    }
+    m->hbuf_bytes = set_bytes;
+  }
+  for (int k = 0; k < 2; ++k)
+    if (!m->hstream[k]) {
+      cudaError_t e = cudaStreamCreateWithFlags(&m->hstream[k], cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_fail(e, "stream create");
+    }
+  int launches = 0;
+  for (int64_t b0 = 0, k = 0; b0 < batch; b0 += chunk, ++k) {
+    const int64_t bc = std::min(chunk, batch - b0);
+    cudaStream_t s = m->hstream[k & 1];
+    double* base = reinterpret_cast<double*>(m->hbuf[k & 1]);
+    double* dq = base;
+    double* dqd = base + (size_t)n * chunk;
+    double* dqdd = base + (size_t)2 * n * chunk;
+    double* dtau = base + (size_t)3 * n * chunk;
+    const size_t hp = (size_t)batch * sizeof(double), dp = (size_t)bc * sizeof(double);
+    cudaError_t e = cudaMemcpy2DAsync(dq, dp, q + b0, hp, dp, n, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpy2DAsync(dqd, dp, qd + b0, hp, dp, n, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpy2DAsync(dqdd, dp, qdd + b0, hp, dp, n, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "host path H2D");
+    m->mu.unlock();
+    st = inverse_dynamics<double>(m, bc, dq, dqd, dqdd, dtau, s);
+    m->mu.lock();
+    launches += g_launches;
+    if (st != RD_OK) return st;
+    e = cudaMemcpy2DAsync(tau + b0, hp, dtau, dp, dp, n, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "host path D2H");
+  }
+  for (int k = 0; k < 2; ++k) {
+    cudaError_t e = cudaStreamSynchronize(m->hstream[k]);
+    if (e != cudaSuccess) return cuda_fail(e, "host path sync");
+  }
+  g_launches = launches;
+  return RD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// rd_internal.h -- host/device shared declarations of librd (product path).
+// No oracle code is included or linked here.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rd {
+
+// Per-link constants in the JOINT frame of each link:
+// the link frame is re-chosen so that S'_i = (beta e_z, alpha e_z), i.e. the
+// joint axis is the local z axis through the origin.  f'_{i-1,i}(q) =
+// (Rm, pm) * (Rz(alpha q), (0, 0, beta q)).  alpha = 1, beta = pitch for a
+// revolute/screw joint; alpha = 0, beta = 1 for a prismatic joint.
+// Spatial inertia J' = [[m I, -[h]], [[h], I]] with h = m c and I the
+// rotational inertia about the (joint-frame) origin, I = {xx, yy, zz, xy, xz, yz}.
+template <typename T>
+struct LinkConst {
+  T Rm[9];      // row-major
+  T pm[3];
+  T m;
+  T h[3];
+  T I[6];
+  T alpha, beta;
+};
+
+// Boundary data of Eq. (3) in the joint frames: V_0, Vdot_0 (base frame,
+// unchanged) and F_{n+1} (expressed in link n's joint frame).
+template <typename T>
+struct Boundary {
+  T V0[6], Vd0[6], Ftip[6];
+};
+
+// Kernel-parameter image for the compile-time-N kernels (lives in the constant
+// bank; every access has a compile-time offset so the DFMAs take it directly).
+template <typename T, int N>
+struct RneaParams {
+  LinkConst<T> L[N];
+  Boundary<T> bnd;
+};
+
+struct ModelHost;   // defined in capi.cu
+
+enum Strategy { kAuto = 0, kThread = 1, kWarpScan = 2, kGeneric = 3 };
+
+// Launchers (rnea_thread.cu / rnea_generic.cu / rnea_warp.cu / aba.cu).
+// All return cudaGetLastError() after enqueue.  `launches` is incremented by
+// the number of kernels enqueued.
+template <typename T>
+cudaError_t launch_rnea_thread(int n, const LinkConst<T>* L_host, const Boundary<T>& bnd,
+                               int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
+                               cudaStream_t st, int* launches, bool* supported);
+template <typename T>
+cudaError_t launch_rnea_generic(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
+                                int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
+                                T* ws, int64_t ws_slots, cudaStream_t st, int* launches);
+template <typename T>
+cudaError_t launch_rnea_warp(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
+                             int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
+                             cudaStream_t st, int* launches, bool* supported);
+template <typename T>
+cudaError_t launch_aba(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
+                       int64_t B, const T* q, const T* qd, const T* tau, T* qdd,
+                       T* ws, int64_t ws_slots, cudaStream_t st, int* launches);
+
+// Workspace slots (threads) the generic / ABA kernels use: ws holds
+// per-link doubles for each slot (see the .cu files for the layout).
+int64_t generic_ws_slots(int64_t B);
+int generic_ws_per_link();
+int aba_ws_per_link();
+
+bool thread_kernel_has_n(int n, bool fp64);
+int num_sms();
+
+}  // namespace rd

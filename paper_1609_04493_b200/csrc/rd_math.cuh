@@ -1,0 +1,142 @@
+// rd_math.cuh -- per-link RNEA arithmetic in joint frames (product path).
+//
+// Notation follows PAPER.md Eq. (1)-(2): V_i, Vdot_i (twists, (v,w)),
+// Fhat_i = J_i Vdot_i - ad^T_{V_i}(J_i V_i), F_i (wrench, (f,m)),
+// tau_i = S_i^T F_i.  In the joint frame of link i, f_{i-1,i} = (R, p) with
+// R = Rm Rz(alpha q), p = pm + beta q Rm e_z, and S_i = (beta e_z, alpha e_z)
+// (DESIGN.md "Joint frames").  Lean forms:
+//   Ad_{f^-1}(v, w)       = (R^T (v + w x p), R^T w)
+//   ad_V(S qd)            = qd (beta w x e_z + alpha v x e_z, alpha w x e_z)
+//   -ad^T_V (P_f, P_m)    = (w x P_f, v x P_f + w x P_m)
+//   J (v, w)              = (m v - h x w, h x v + I w)
+//   Ad^T_{f^-1}(f, m)     = (R f, p x (R f) + R m)
+#pragma once
+#include "rd_internal.h"
+
+namespace rd {
+
+template <typename T>
+struct Rot {
+  T r00, r01, r02, r10, r11, r12, r20, r21, r22;
+};
+
+__device__ __forceinline__ void rd_sincos(double x, double* s, double* c) { sincos(x, s, c); }
+__device__ __forceinline__ void rd_sincos(float x, float* s, float* c) { sincosf(x, s, c); }
+
+// R = Rm * Rz(theta) from (s, c) = (sin theta, cos theta): only the first two
+// columns change, R[:,2] = Rm[:,2].
+template <typename T>
+__device__ __forceinline__ Rot<T> make_rot(const LinkConst<T>& C, T s, T c) {
+  Rot<T> R;
+  R.r00 = fma(C.Rm[0], c, C.Rm[1] * s);
+  R.r10 = fma(C.Rm[3], c, C.Rm[4] * s);
+  R.r20 = fma(C.Rm[6], c, C.Rm[7] * s);
+  R.r01 = fma(C.Rm[1], c, -(C.Rm[0] * s));
+  R.r11 = fma(C.Rm[4], c, -(C.Rm[3] * s));
+  R.r21 = fma(C.Rm[7], c, -(C.Rm[6] * s));
+  R.r02 = C.Rm[2];
+  R.r12 = C.Rm[5];
+  R.r22 = C.Rm[8];
+  return R;
+}
+
+// y = R^T x
+template <typename T>
+__device__ __forceinline__ void rot_t(const Rot<T>& R, T x0, T x1, T x2, T& y0, T& y1, T& y2) {
+  y0 = fma(R.r00, x0, fma(R.r10, x1, R.r20 * x2));
+  y1 = fma(R.r01, x0, fma(R.r11, x1, R.r21 * x2));
+  y2 = fma(R.r02, x0, fma(R.r12, x1, R.r22 * x2));
+}
+// y = R x
+template <typename T>
+__device__ __forceinline__ void rot_n(const Rot<T>& R, T x0, T x1, T x2, T& y0, T& y1, T& y2) {
+  y0 = fma(R.r00, x0, fma(R.r01, x1, R.r02 * x2));
+  y1 = fma(R.r10, x0, fma(R.r11, x1, R.r12 * x2));
+  y2 = fma(R.r20, x0, fma(R.r21, x1, R.r22 * x2));
+}
+
+// out = Ad_{f^-1} in, with f = (R, p):  (R^T (v + w x p), R^T w)
+template <typename T>
+__device__ __forceinline__ void ad_finv(const Rot<T>& R, T p0, T p1, T p2, const T* in, T* out) {
+  const T x0 = fma(in[4], p2, fma(-in[5], p1, in[0]));
+  const T x1 = fma(in[5], p0, fma(-in[3], p2, in[1]));
+  const T x2 = fma(in[3], p1, fma(-in[4], p0, in[2]));
+  rot_t(R, x0, x1, x2, out[0], out[1], out[2]);
+  rot_t(R, in[3], in[4], in[5], out[3], out[4], out[5]);
+}
+
+// Fhat = J Vd + (w x P_f, v x P_f + w x P_m), P = J V
+template <typename T>
+__device__ __forceinline__ void bias_force(const LinkConst<T>& C, const T* V, const T* Vd, T* Fh) {
+  const T m = C.m, h0 = C.h[0], h1 = C.h[1], h2 = C.h[2];
+  const T Ixx = C.I[0], Iyy = C.I[1], Izz = C.I[2], Ixy = C.I[3], Ixz = C.I[4], Iyz = C.I[5];
+  // P = J V
+  const T Pf0 = fma(m, V[0], fma(-h1, V[5], h2 * V[4]));
+  const T Pf1 = fma(m, V[1], fma(-h2, V[3], h0 * V[5]));
+  const T Pf2 = fma(m, V[2], fma(-h0, V[4], h1 * V[3]));
+  const T Pm0 = fma(h1, V[2], fma(-h2, V[1], fma(Ixx, V[3], fma(Ixy, V[4], Ixz * V[5]))));
+  const T Pm1 = fma(h2, V[0], fma(-h0, V[2], fma(Ixy, V[3], fma(Iyy, V[4], Iyz * V[5]))));
+  const T Pm2 = fma(h0, V[1], fma(-h1, V[0], fma(Ixz, V[3], fma(Iyz, V[4], Izz * V[5]))));
+  // A = J Vd, then add the gyroscopic terms
+  T Af0 = fma(m, Vd[0], fma(-h1, Vd[5], h2 * Vd[4]));
+  T Af1 = fma(m, Vd[1], fma(-h2, Vd[3], h0 * Vd[5]));
+  T Af2 = fma(m, Vd[2], fma(-h0, Vd[4], h1 * Vd[3]));
+  T Am0 = fma(h1, Vd[2], fma(-h2, Vd[1], fma(Ixx, Vd[3], fma(Ixy, Vd[4], Ixz * Vd[5]))));
+  T Am1 = fma(h2, Vd[0], fma(-h0, Vd[2], fma(Ixy, Vd[3], fma(Iyy, Vd[4], Iyz * Vd[5]))));
+  T Am2 = fma(h0, Vd[1], fma(-h1, Vd[0], fma(Ixz, Vd[3], fma(Iyz, Vd[4], Izz * Vd[5]))));
+  const T w0 = V[3], w1 = V[4], w2 = V[5], v0 = V[0], v1 = V[1], v2 = V[2];
+  Fh[0] = fma(w1, Pf2, fma(-w2, Pf1, Af0));
+  Fh[1] = fma(w2, Pf0, fma(-w0, Pf2, Af1));
+  Fh[2] = fma(w0, Pf1, fma(-w1, Pf0, Af2));
+  Fh[3] = fma(v1, Pf2, fma(-v2, Pf1, fma(w1, Pm2, fma(-w2, Pm1, Am0))));
+  Fh[4] = fma(v2, Pf0, fma(-v0, Pf2, fma(w2, Pm0, fma(-w0, Pm2, Am1))));
+  Fh[5] = fma(v0, Pf1, fma(-v1, Pf0, fma(w0, Pm1, fma(-w1, Pm0, Am2))));
+}
+
+// One forward step of Eq. (1) for link with constants C:
+//   V  = Ad_{f^-1} Vp + S qd
+//   Vd = Ad_{f^-1} Vdp + S qdd + ad_V (S qd)      (= ... - ad_{S qd} Ad_{f^-1} Vp)
+// REV: alpha = 1, beta = 0 known at compile time.
+template <typename T, bool REV>
+__device__ __forceinline__ void fwd_step(const LinkConst<T>& C, const Rot<T>& R, T p0, T p1, T p2,
+                                         T qd, T qdd, const T* Vp, const T* Vdp, T* V, T* Vd) {
+  ad_finv(R, p0, p1, p2, Vp, V);
+  ad_finv(R, p0, p1, p2, Vdp, Vd);
+  if (REV) {
+    V[5] += qd;
+    Vd[5] += qdd;
+    // ad_V(e_z qd) = qd (v x e_z, w x e_z),  a x e_z = (a1, -a0, 0)
+    Vd[0] = fma(qd, V[1], Vd[0]);
+    Vd[1] = fma(-qd, V[0], Vd[1]);
+    Vd[3] = fma(qd, V[4], Vd[3]);
+    Vd[4] = fma(-qd, V[3], Vd[4]);
+  } else {
+    const T a = C.alpha, b = C.beta;
+    V[2] = fma(b, qd, V[2]);
+    V[5] = fma(a, qd, V[5]);
+    Vd[2] = fma(b, qdd, Vd[2]);
+    Vd[5] = fma(a, qdd, Vd[5]);
+    const T aq = a * qd, bq = b * qd;
+    Vd[0] = fma(bq, V[4], fma(aq, V[1], Vd[0]));
+    Vd[1] = fma(-bq, V[3], fma(-aq, V[0], Vd[1]));
+    Vd[3] = fma(aq, V[4], Vd[3]);
+    Vd[4] = fma(-aq, V[3], Vd[4]);
+  }
+}
+
+// One backward step of Eq. (2): F = Fhat + Ad^T_{f_{i,i+1}^{-1}} Fn
+// where (R, p) is the transform of link i+1.
+template <typename T>
+__device__ __forceinline__ void bwd_step(const Rot<T>& R, T p0, T p1, T p2, const T* Fn, const T* Fh, T* F) {
+  T y0, y1, y2, z0, z1, z2;
+  rot_n(R, Fn[0], Fn[1], Fn[2], y0, y1, y2);
+  rot_n(R, Fn[3], Fn[4], Fn[5], z0, z1, z2);
+  F[0] = Fh[0] + y0;
+  F[1] = Fh[1] + y1;
+  F[2] = Fh[2] + y2;
+  F[3] = fma(p1, y2, fma(-p2, y1, Fh[3] + z0));
+  F[4] = fma(p2, y0, fma(-p0, y2, Fh[4] + z1));
+  F[5] = fma(p0, y1, fma(-p1, y0, Fh[5] + z2));
+}
+
+}  // namespace rd

@@ -1,0 +1,260 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star, A13): per state
+max_i |x_gpu - x_oracle| / max_i |x_oracle| <= 1e-10 (fp64), <= 1e-4 (fp32).
+FD is judged by backward error (A14) plus a cond-scaled forward error.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from conftest import rel_err_per_state
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float64: 1e-10, torch.float32: 1e-4}
+
+
+@pytest.fixture(scope="module")
+def rd():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1609_04493_b200 as rd
+    rd.lib()
+    return rd
+
+
+def dev(x, dtype=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dtype=dtype)
+
+
+def run_id(rd, model, q, qd, qdd, dtype=torch.float64):
+    tq, tqd, tqdd = dev(q, dtype), dev(qd, dtype), dev(qdd, dtype)
+    tau = rd.inverse_dynamics(model, tq, tqd, tqdd)
+    torch.cuda.synchronize()
+    # the oracle sees exactly the (rounded) inputs the kernel saw
+    return tau.double().cpu().numpy(), (tq.double().cpu().numpy(), tqd.double().cpu().numpy(),
+                                        tqdd.double().cpu().numpy())
+
+
+def check_id(rd, robot, g, q, qd, qdd, dtype=torch.float64, strategy="auto", sample=None):
+    model = rd.Model.from_robot(robot, g)
+    model.set_strategy(strategy)
+    tau, (q64, qd64, qdd64) = run_id(rd, model, q, qd, qdd, dtype)
+    cols = np.arange(q.shape[1]) if sample is None else sample
+    ref = oracle.rnea_batch(robot, g, q64[:, cols], qd64[:, cols], qdd64[:, cols])
+    err = rel_err_per_state(tau[:, cols], ref)
+    assert np.all(np.isfinite(tau[:, cols]))
+    assert err.max() <= TOL[dtype], f"max rel err {err.max():.3e} (strategy {strategy}, {dtype})"
+    return err.max()
+
+
+# ------------------------------------------------------------------ configs
+def test_C1_planar2_closed_form_config(rd):
+    cfg = synth.CONFIGS["C1"]
+    q, qd, qdd = synth.states(cfg["seed"], 2, 0, cfg["batch"], cfg["ranges"])
+    for strat in ("auto", "thread", "generic"):
+        check_id(rd, synth.planar2(), cfg["gravity"], q, qd, qdd, strategy=strat)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_C2_arm7(rd, dtype):
+    cfg = synth.CONFIGS["C2"]
+    q, qd, qdd = synth.states(cfg["seed"], 7, 0, cfg["batch"], cfg["ranges"])
+    for strat in ("thread", "generic"):
+        check_id(rd, synth.arm7(), cfg["gravity"], q, qd, qdd, dtype, strategy=strat)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_C3_full_size_sampled(rd, dtype):
+    # Full 1M-state launch (the bench configuration), sampled oracle comparison:
+    # first/last 1024, every 128-state tile boundary neighbourhood, and random states.
+    cfg = synth.CONFIGS["C3"]
+    n, B = cfg["n"], cfg["batch"]
+    q, qd, qdd = synth.states(cfg["seed"], n, 0, B, cfg["ranges"])
+    rng = np.random.default_rng(99)
+    sample = np.unique(np.concatenate([np.arange(1024), np.arange(B - 1024, B),
+                                       rng.integers(0, B, 8192), np.arange(127, B, 128 * 997)]))
+    check_id(rd, synth.robot_for(cfg), cfg["gravity"], q, qd, qdd, dtype, sample=sample)
+
+
+@pytest.mark.parametrize("strategy", ["thread", "generic"])
+def test_C3_small_all_states(rd, strategy):
+    cfg = synth.CONFIGS["C3"]
+    q, qd, qdd = synth.states(cfg["seed"], 30, 0, 3000, cfg["ranges"])
+    check_id(rd, synth.robot_for(cfg), cfg["gravity"], q, qd, qdd, strategy=strategy)
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("B", [1, 2, 31, 127, 128, 129, 1000, 4097])
+def test_ragged_batches(rd, B):
+    r = synth.random_chain(30, 1030)
+    q, qd, qdd = synth.states(7, 30, 0, B)
+    check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd)
+
+
+def test_empty_batch_is_noop(rd):
+    model = rd.Model.from_robot(synth.random_chain(6, 1), synth.GRAVITY_Z)
+    z = torch.empty((6, 0), dtype=torch.float64, device="cuda")
+    rd.inverse_dynamics(model, z, z, z, out=torch.empty((6, 0), dtype=torch.float64, device="cuda"))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 6, 7, 10, 13, 30, 64, 100])
+def test_link_counts_random_chains(rd, n):
+    r = synth.random_chain(n, 500 + n)
+    q, qd, qdd = synth.states(11, n, 0, 777)
+    for strat in ("auto", "generic"):
+        check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strat)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_prismatic_and_screw_joints_generic(rd, dtype):
+    r = synth.random_chain(12, 77, prismatic_fraction=0.5)
+    # add a screw pitch to one revolute joint: v += 0.2 w
+    for i in range(12):
+        if np.linalg.norm(r["S"][i, 3:]) > 0.5:
+            r["S"][i, :3] += 0.2 * r["S"][i, 3:]
+            break
+    q, qd, qdd = synth.states(12, 12, 0, 2000)
+    check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype)
+
+
+def test_pendulum_closed_form_on_gpu(rd):
+    m, l, Izz, g = 1.7, 0.8, 0.05, 9.81
+    model = rd.Model.from_robot(synth.pendulum(m, l, Izz), (0, -g, 0))
+    q, qd, qdd = synth.states(3, 1, 0, 5000, "C1")
+    tau = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd)).cpu().numpy()
+    ref = (m * l * l + Izz) * qdd + m * g * l * np.cos(q)
+    assert np.abs(tau - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_full_boundary_V0_Vdot0_Ftip(rd):
+    # NEXT-4: non-zero V_0, Vdot_0, F_{n+1} (Eq. 3 full signature)
+    r = synth.random_chain(7, 31, prismatic_fraction=0.3)
+    rng = np.random.default_rng(5)
+    V0, Vd0, Ft = rng.standard_normal((3, 6))
+    model = rd.Model.from_robot(r, (0, 0, 0))
+    model.set_boundary(V0, Vd0, Ft)
+    q, qd, qdd = synth.states(13, 7, 0, 300)
+    for strat in ("generic",):
+        model.set_strategy(strat)
+        tau = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd)).cpu().numpy()
+        ref = np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b], V0, Vd0, Ft) for b in range(300)], 1)
+        assert rel_err_per_state(tau, ref).max() <= 1e-10
+    r2 = synth.random_chain(7, 32)                 # all revolute -> thread kernel
+    model2 = rd.Model.from_robot(r2, (0, 0, 0))
+    model2.set_boundary(V0, Vd0, Ft)
+    for strat in ("thread", "generic"):
+        model2.set_strategy(strat)
+        tau = rd.inverse_dynamics(model2, dev(q), dev(qd), dev(qdd)).cpu().numpy()
+        ref = np.stack([oracle.rnea(r2, q[:, b], qd[:, b], qdd[:, b], V0, Vd0, Ft) for b in range(300)], 1)
+        assert rel_err_per_state(tau, ref).max() <= 1e-10
+
+
+def test_deterministic_and_strategy_consistent(rd):
+    cfg = synth.CONFIGS["C3"]
+    q, qd, qdd = synth.states(cfg["seed"], 30, 0, 20000)
+    model = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
+    a = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd))
+    b = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd))
+    assert torch.equal(a, b)                       # bit-identical repeat
+    # a shard evaluated alone equals the same states inside the full batch
+    c = rd.inverse_dynamics(model, dev(q[:, 5000:9000]), dev(qd[:, 5000:9000]), dev(qdd[:, 5000:9000]))
+    assert torch.equal(a[:, 5000:9000], c)
+
+
+def test_host_path_equals_device_path(rd):
+    cfg = synth.CONFIGS["C3"]
+    q, qd, qdd = synth.states(cfg["seed"], 30, 0, 50000)
+    model = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
+    dev_tau = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd)).cpu().numpy()
+    host_tau = rd.inverse_dynamics_host(model, q, qd, qdd)
+    np.testing.assert_array_equal(host_tau, dev_tau)
+    pq, pqd, pqdd = (torch.from_numpy(x).pin_memory() for x in (q, qd, qdd))
+    out = torch.empty_like(pq).pin_memory()
+    rd.inverse_dynamics_host(model, pq, pqd, pqdd, out)
+    np.testing.assert_array_equal(out.numpy(), dev_tau)
+
+
+def test_launch_count_and_errors(rd):
+    model = rd.Model.from_robot(synth.random_chain(30, 1030), synth.GRAVITY_Z)
+    q = torch.zeros((30, 1000), dtype=torch.float64, device="cuda")
+    rd.inverse_dynamics(model, q, q, q)
+    assert rd.last_launch_count() == 1
+    with pytest.raises(rd.RdError):
+        rd.inverse_dynamics(model, q, q, q, out=q)                    # aliasing
+    with pytest.raises(rd.RdError):
+        rd.inverse_dynamics(model, q.cpu(), q.cpu(), q.cpu())          # host tensors on device API
+
+
+# ------------------------------------------------------------------ forward dynamics (ABA)
+def check_fd(rd, robot, g, B, seed, dtype=torch.float64, bwd_tol=1e-10):
+    n = robot["S"].shape[0]
+    q, qd, qdd = synth.states(seed, n, 0, B)
+    if dtype == torch.float32:
+        q, qd, qdd = (x.astype(np.float32).astype(np.float64) for x in (q, qd, qdd))
+    tau = oracle.rnea_batch(robot, g, q, qd, qdd)
+    if dtype == torch.float32:
+        tau = tau.astype(np.float32).astype(np.float64)
+    model = rd.Model.from_robot(robot, g)
+    out = rd.forward_dynamics(model, dev(q, dtype), dev(qd, dtype), dev(tau, dtype)).double().cpu().numpy()
+    assert np.all(np.isfinite(out))
+    back = oracle.rnea_batch(robot, g, q, qd, out)       # backward error (A14)
+    berr = rel_err_per_state(back, tau)
+    assert berr.max() <= bwd_tol, f"FD backward error {berr.max():.3e}"
+    fwd = oracle.fd_batch(robot, g, q, qd, tau)
+    ferr = rel_err_per_state(out, fwd, floor=1.0)
+    return berr.max(), ferr.max()
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 30])
+def test_fd_aba_parity(rd, n):
+    r = synth.random_chain(n, 900 + n, prismatic_fraction=0.3 if n < 30 else 0.0)
+    b, f = check_fd(rd, r, synth.GRAVITY_Z, 2000, 4)
+    assert f < 1e-8
+
+
+def test_fd_C4_sampled(rd):
+    # Config C4: n = 100, 100k states (the bench launch); sampled backward-error check.
+    cfg = synth.CONFIGS["C4"]
+    r = synth.robot_for(cfg)
+    n, B = cfg["n"], cfg["batch"]
+    q, qd, qdd = synth.states(cfg["seed"], n, 0, B)
+    sample = np.unique(np.concatenate([np.arange(256), np.arange(B - 256, B),
+                                       np.random.default_rng(99).integers(0, B, 2048)]))
+    tau_s = oracle.rnea_batch(r, cfg["gravity"], q[:, sample], qd[:, sample], qdd[:, sample])
+    tau = np.zeros((n, B))
+    tau[:, sample] = tau_s
+    model = rd.Model.from_robot(r, cfg["gravity"])
+    out = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()
+    back = oracle.rnea_batch(r, cfg["gravity"], q[:, sample], qd[:, sample], out[:, sample])
+    assert rel_err_per_state(back, tau_s).max() <= 1e-10
+
+
+def test_fd_fp32(rd):
+    r = synth.random_chain(7, 907)
+    check_fd(rd, r, synth.GRAVITY_Z, 2000, 5, torch.float32, bwd_tol=1e-4)
+
+
+def test_fd_pendulum_closed_form(rd):
+    m, l, g = 1.3, 0.9, 9.81
+    model = rd.Model.from_robot(synth.pendulum(m, l, 1e-9), (0, -g, 0))
+    q, qd, _ = synth.states(6, 1, 0, 1000)
+    out = rd.forward_dynamics(model, dev(q), dev(qd), dev(np.zeros_like(q))).cpu().numpy()
+    ref = -(m * g * l * np.cos(q)) / (m * l * l + 1e-9)
+    assert np.abs(out - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+def test_fd_tip_wrench(rd):
+    r = synth.random_chain(6, 41)
+    rng = np.random.default_rng(1)
+    Ft = rng.standard_normal(6)
+    model = rd.Model.from_robot(r, synth.GRAVITY_Z)
+    model.set_boundary(None, None, Ft)
+    q, qd, qdd = synth.states(8, 6, 0, 200)
+    Vd0 = np.concatenate([-synth.GRAVITY_Z, np.zeros(3)])
+    tau = np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b], None, Vd0, Ft) for b in range(200)], 1)
+    out = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()
+    assert rel_err_per_state(out, qdd, floor=1.0).max() < 1e-9
