@@ -20,8 +20,61 @@ struct Rot {
   T r00, r01, r02, r10, r11, r12, r20, r21, r22;
 };
 
-__device__ __forceinline__ void rd_sincos(double x, double* s, double* c) { sincos(x, s, c); }
-__device__ __forceinline__ void rd_sincos(float x, float* s, float* c) { sincosf(x, s, c); }
+// sin/cos of a joint angle, branch-free (one basic block, so the scheduler can
+// interleave it with the V/Vdot chains).  Quadrant k = rint(2x/pi) by the
+// 1.5*2^52 rounding trick; Cody-Waite reduction with pi/2 split in two doubles
+// (each FMA rounds once, the split carries ~107 bits of pi/2, so the reduced
+// argument is accurate to ~1 ulp for |x| up to ~1e9); fdlibm minimax
+// polynomials (__kernel_sin / __kernel_cos coefficients) on [-pi/4, pi/4].
+// Measured against the host libm in tests/test_gpu_parity.py (large-angle case).
+__device__ __forceinline__ void rd_sincos(double x, double* sp, double* cp) {
+  {
+    const double kRound = 6755399441055744.0;              // 1.5 * 2^52
+    const double t = fma(x, 0.63661977236758138, kRound);
+    const int quad = __double2loint(t);
+    const double k = t - kRound;
+    double r = fma(-k, 1.5707963267948966, x);
+    r = fma(-k, 6.123233995736766e-17, r);
+    const double z = r * r;
+    double ps = fma(z, 1.58969099521155010221e-10, -2.50507602534068634195e-08);
+    ps = fma(z, ps, 2.75573137070700676789e-06);
+    ps = fma(z, ps, -1.98412698298579493134e-04);
+    ps = fma(z, ps, 8.33333333332248946124e-03);
+    ps = fma(z, ps, -1.66666666666666324348e-01);
+    const double sn = fma(z * r, ps, r);
+    double pc = fma(z, -1.13596475577881948265e-11, 2.08757232129817482790e-09);
+    pc = fma(z, pc, -2.75573143513906633035e-07);
+    pc = fma(z, pc, 2.48015872894767294178e-05);
+    pc = fma(z, pc, -1.38888888888741095749e-03);
+    pc = fma(z, pc, 4.16666666666666019037e-02);
+    const double cs = fma(z * z, pc, fma(-0.5, z, 1.0));
+    // sin(x) = [s, c, -s, -c][quad & 3], cos(x) = [c, -s, -c, s][quad & 3]
+    const double a = (quad & 1) ? cs : sn;
+    const double b = (quad & 1) ? sn : cs;
+    *sp = (quad & 2) ? -a : a;
+    *cp = ((quad + 1) & 2) ? -b : b;
+  }
+}
+// fp32: three-float Cody-Waite split of pi/2 (accurate for |x| up to ~1e4) and
+// Cephes minimax polynomials; branch-free.
+__device__ __forceinline__ void rd_sincos(float x, float* sp, float* cp) {
+  {
+    const float k = rintf(x * 0.636619772f);
+    const int quad = (int)k;
+    float r = fmaf(-k, 1.57079637f, x);                 // pi/2 in three floats (Cody-Waite)
+    r = fmaf(-k, -4.37113883e-08f, r);
+    r = fmaf(-k, -1.71512489e-15f, r);
+    const float z = r * r;
+    // minimax on [-pi/4, pi/4] (Cephes sinf/cosf coefficients)
+    const float sn = fmaf(z * r, fmaf(z, fmaf(z, -1.9515295891e-4f, 8.3321608736e-3f), -1.6666654611e-1f), r);
+    const float cs = fmaf(z * z, fmaf(z, fmaf(z, 2.443315711809948e-5f, -1.388731625493765e-3f),
+                                       4.166664568298827e-2f), fmaf(-0.5f, z, 1.0f));
+    const float a = (quad & 1) ? cs : sn;
+    const float b = (quad & 1) ? sn : cs;
+    *sp = (quad & 2) ? -a : a;
+    *cp = ((quad + 1) & 2) ? -b : b;
+  }
+}
 
 // R = Rm * Rz(theta) from (s, c) = (sin theta, cos theta): only the first two
 // columns change, R[:,2] = Rm[:,2].

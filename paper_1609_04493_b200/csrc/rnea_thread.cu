@@ -1,15 +1,21 @@
-// rnea_thread.cu -- one thread per state, serial RNEA (Eq. 1-2, P:60-78;
-// Alg. 1 P:403-418 collapsed to one pass per state), compile-time N.
+// rnea_thread.cu -- one thread per state, serial RNEA (Eq. 1-2; the two
+// scans of Alg. 1, run as one forward and one backward sweep per
+// state), for n <= 32 links.
 //
-// Each thread runs the forward recursion over links 1..n (transform, V, Vdot,
-// Fhat), stashes per link (sin q, cos q, Fhat) = 8 scalars, then runs the
-// backward wrench recursion n..1 and stores tau.  The stash lives in
-//   * TMEM  (kTmem): tcgen05.st / tcgen05.ld, 2 KB per thread lane, 128
-//     threads per CTA (one per TMEM lane), one persistent CTA per SM;
-//   * local (kLocal): a per-thread array the compiler keeps in registers /
-//     spills to local memory (L1);
-// (DESIGN.md "Kernels: rnea_thread").  Model constants are a __grid_constant__
-// kernel parameter, so every access is a constant-bank operand.
+// Design:
+//  * one persistent CTA per SM, W warps (W = 8 or 16), looping over tiles of
+//    32*W states; one thread per state;
+//  * the per-link stash the backward sweep needs, (sin q, cos q, Fhat) = 8
+//    scalars, lives ON CHIP: the first `lt` links in Tensor Memory (tcgen05.st /
+//    tcgen05.ld, 32x32b shape: warp w owns TMEM lanes 32(w%4).., and columns
+//    [(w/4) * 2048/W, ...)), the remaining n - lt links in shared memory laid
+//    out [link][8][thread] (conflict-free, 256 B per warp access);
+//  * model constants are a __grid_constant__ kernel parameter indexed by the
+//    (warp-uniform) link counter: uniform constant-bank loads;
+//  * inputs q, qd, qdd are read coalesced (x[i*B + b]) two links ahead of use;
+//    tau is written coalesced during the backward sweep;
+//  * the loops are rolled (unroll 2): the whole kernel stays in the instruction
+//    cache (a fully unrolled n = 30 body thrashed it, profiles/r01).
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdlib>
@@ -18,27 +24,35 @@
 
 namespace rd {
 
-enum StashKind { kLocal = 0, kTmem = 1 };
+constexpr int kMaxThreadN = 32;
 
-// ------------------------------------------------------------------ TMEM stash
+template <typename T>
+struct ThreadParams {
+  LinkConst<T> L[kMaxThreadN];
+  Boundary<T> bnd;
+  int n;          // links
+  int lt;         // links stashed in TMEM (the rest in shared memory)
+};
+
+// ------------------------------------------------------------------ TMEM helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
 __device__ __forceinline__ void tmem_alloc_512(uint32_t* slot_smem) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n"
-               :: "r"(smem_u32(slot_smem)));
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" :: "r"(smem_u32(slot_smem)));
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
 }
 __device__ __forceinline__ void tmem_dealloc_512(uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" :: "r"(taddr));
 }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
-// 8 scalars of type T -> 16 (double) or 8 (float) 32-bit TMEM columns.
+// 8 scalars of type T <-> 16 (fp64) or 8 (fp32) 32-bit TMEM columns of this thread's lane.
 template <typename T> struct TmemIO;
 
 template <> struct TmemIO<double> {
   static constexpr int kCols = 16;
+  typedef uint32_t Regs[16];
   __device__ static __forceinline__ void st(uint32_t a, const double* v) {
     uint32_t r[16];
 #pragma unroll
@@ -58,8 +72,7 @@ template <> struct TmemIO<double> {
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(a));
   }
-  // Completes the outstanding tcgen05.ld; the "+r" operands order every use of
-  // the loaded registers after the wait.
+  // Completes outstanding tcgen05.ld; "+r" orders every use of r after the wait.
   __device__ static __forceinline__ void wait(uint32_t* r) {
     asm volatile("tcgen05.wait::ld.sync.aligned;\n"
                  : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
@@ -73,18 +86,17 @@ template <> struct TmemIO<double> {
 
 template <> struct TmemIO<float> {
   static constexpr int kCols = 8;
+  typedef uint32_t Regs[8];
   __device__ static __forceinline__ void st(uint32_t a, const float* v) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n"
-        :: "r"(a), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-           "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-           "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n"
+                 :: "r"(a), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                    "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                    "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
   }
   __device__ static __forceinline__ void ld(uint32_t a, uint32_t* r) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-        : "r"(a));
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(a));
   }
   __device__ static __forceinline__ void wait(uint32_t* r) {
     asm volatile("tcgen05.wait::ld.sync.aligned;\n"
@@ -96,127 +108,324 @@ template <> struct TmemIO<float> {
   }
 };
 
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
-
-// ------------------------------------------------------------------ kernel body
-// Processes state b (clamped for loads when b >= B; tau stored only if b < B).
-template <typename T, int N, int STASH>
-__device__ __forceinline__ void rnea_one_state(const RneaParams<T, N>& P, int64_t B, int64_t b,
-                                               const T* __restrict__ q, const T* __restrict__ qd,
-                                               const T* __restrict__ qdd, T* __restrict__ tau,
-                                               uint32_t tbase) {
-  const bool valid = b < B;
-  const int64_t bl = valid ? b : (B - 1);
-  constexpr int PF = 3;                 // input prefetch distance (links)
-  T pq[PF], pd[PF], pa[PF];
-#pragma unroll
-  for (int k = 0; k < PF; ++k) {
-    if (k < N) {
-      pq[k] = __ldg(q + (int64_t)k * B + bl);
-      pd[k] = __ldg(qd + (int64_t)k * B + bl);
-      pa[k] = __ldg(qdd + (int64_t)k * B + bl);
-    }
-  }
-  T local_stash[STASH == kLocal ? N : 1][8];
-  (void)local_stash;
-
-  T V[6], Vd[6];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) { V[k] = P.bnd.V0[k]; Vd[k] = P.bnd.Vd0[k]; }
-
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const T qi = pq[i % PF], qdi = pd[i % PF], qddi = pa[i % PF];
-    if (i + PF < N) {
-      pq[i % PF] = __ldg(q + (int64_t)(i + PF) * B + bl);
-      pd[i % PF] = __ldg(qd + (int64_t)(i + PF) * B + bl);
-      pa[i % PF] = __ldg(qdd + (int64_t)(i + PF) * B + bl);
-    }
-    const LinkConst<T>& C = P.L[i];
-    T s, c;
-    rd_sincos(qi, &s, &c);
-    const Rot<T> R = make_rot(C, s, c);
-    T Vn[6], Vdn[6];
-    fwd_step<T, true>(C, R, C.pm[0], C.pm[1], C.pm[2], qdi, qddi, V, Vd, Vn, Vdn);
-    T st[8];
-    st[0] = s;
-    st[1] = c;
-    bias_force(C, Vn, Vdn, st + 2);
-    if (STASH == kLocal) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) local_stash[STASH == kLocal ? i : 0][k] = st[k];
-    } else {
-      TmemIO<T>::st(tbase + (uint32_t)(i * TmemIO<T>::kCols), st);
-    }
-#pragma unroll
-    for (int k = 0; k < 6; ++k) { V[k] = Vn[k]; Vd[k] = Vdn[k]; }
-  }
-
-  // Backward recursion, Eq. (2): F_n = Fhat_n + F_{n+1} (f_{n,n+1} = I, A5),
-  // F_i = Fhat_i + Ad^T_{f_{i,i+1}^{-1}} F_{i+1}; tau_i = S_i^T F_i = F_i[5] (joint frame).
-  T F[6];
-  Rot<T> Rn;                           // rotation of link i+1 (rebuilt from its stash)
-  uint32_t rr[2][16];
-  if (STASH == kTmem) {
-    tmem_wait_st();
-    TmemIO<T>::ld(tbase + (uint32_t)((N - 1) * TmemIO<T>::kCols), rr[(N - 1) & 1]);
-  }
-#pragma unroll
-  for (int i = N - 1; i >= 0; --i) {
-    T cur[8];
-    if (STASH == kLocal) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) cur[k] = local_stash[STASH == kLocal ? i : 0][k];
-    } else {
-      TmemIO<T>::wait(rr[i & 1]);
-      TmemIO<T>::unpack(rr[i & 1], cur);
-      if (i > 0) TmemIO<T>::ld(tbase + (uint32_t)((i - 1) * TmemIO<T>::kCols), rr[(i - 1) & 1]);
-    }
-    if (i == N - 1) {
-#pragma unroll
-      for (int k = 0; k < 6; ++k) F[k] = cur[2 + k] + P.bnd.Ftip[k];
-    } else {
-      const LinkConst<T>& Cn = P.L[i + 1];
-      T Fo[6];
-      bwd_step(Rn, Cn.pm[0], Cn.pm[1], Cn.pm[2], F, cur + 2, Fo);
-#pragma unroll
-      for (int k = 0; k < 6; ++k) F[k] = Fo[k];
-    }
-    if (valid) tau[(int64_t)i * B + b] = F[5];
-    if (i > 0) Rn = make_rot(P.L[i], cur[0], cur[1]);
-  }
-}
-
-// Local-stash kernel: one state per thread, plain grid.
-template <typename T, int N>
-__global__ void __launch_bounds__(128)
-rnea_thread_local_kernel(const __grid_constant__ RneaParams<T, N> P, int64_t B,
-                         const T* __restrict__ q, const T* __restrict__ qd,
-                         const T* __restrict__ qdd, T* __restrict__ tau) {
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  rnea_one_state<T, N, kLocal>(P, B, b, q, qd, qdd, tau, 0u);
-}
-
-// TMEM-stash kernel: 128 threads (4 warps = the 4 TMEM lane quarters), one
-// persistent CTA per SM looping over 128-state tiles.  Thread t of warp w owns
-// TMEM lane 32w + t; link i's stash occupies columns [i*kCols, (i+1)*kCols).
-template <typename T, int N>
-__global__ void __launch_bounds__(128, 1)
-rnea_thread_tmem_kernel(const __grid_constant__ RneaParams<T, N> P, int64_t B,
-                        const T* __restrict__ q, const T* __restrict__ qd,
-                        const T* __restrict__ qdd, T* __restrict__ tau) {
-  static_assert(N * TmemIO<T>::kCols <= 512, "stash exceeds the 512 TMEM columns");
+// ------------------------------------------------------------------ kernel
+// W warps per CTA; one CTA per SM (it owns all 512 TMEM columns).
+template <typename T, int W>
+__global__ void __launch_bounds__(W * 32, 1)
+rnea_thread_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
+                   const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
+                   T* __restrict__ tau) {
+  constexpr int NT = W * 32;
+  constexpr int kColsPerWarp = 2048 / W;          // 512 columns x 4 lane quarters / W warps
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sstash = reinterpret_cast<T*>(smem_raw);     // [n - lt][8][NT]
   __shared__ uint32_t tmem_slot;
+
   const int warp = threadIdx.x >> 5;
+  const int tid = threadIdx.x;
   if (warp == 0) tmem_alloc_512(&tmem_slot);
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tbase = tmem_slot + ((uint32_t)(warp * 32) << 16);
-  const int64_t ntiles = (B + 127) / 128;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    rnea_one_state<T, N, kTmem>(P, B, t * 128 + threadIdx.x, q, qd, qdd, tau, tbase);
+  const uint32_t tbase = tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * kColsPerWarp);
+
+  const int n = P.n, lt = P.lt;
+  const int64_t ntiles = (B + NT - 1) / NT;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t b = tile * NT + tid;
+    const bool valid = b < B;
+    const int64_t bl = valid ? b : (B - 1);       // clamped: every lane joins the .sync.aligned TMEM ops
+    const T* pq = q + bl;
+    const T* pqd = qd + bl;
+    const T* pqa = qdd + bl;
+
+    // ---------------- forward sweep, Eq. (1): f_i, V_i, Vdot_i, then Fhat_i
+    T V[6], Vd[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) { V[k] = P.bnd.V0[k]; Vd[k] = P.bnd.Vd0[k]; }
+    T c_q = __ldg(pq), c_qd = __ldg(pqd), c_qa = __ldg(pqa);
+    const int64_t off1 = (n > 1 ? 1 : 0) * B;
+    T n_q = __ldg(pq + off1), n_qd = __ldg(pqd + off1), n_qa = __ldg(pqa + off1);
+#pragma unroll 2
+    for (int i = 0; i < n; ++i) {
+      const int64_t off2 = (int64_t)min(i + 2, n - 1) * B;
+      const T f_q = __ldg(pq + off2), f_qd = __ldg(pqd + off2), f_qa = __ldg(pqa + off2);
+      const LinkConst<T>& C = P.L[i];
+      T s, c;
+      rd_sincos(c_q, &s, &c);
+      const Rot<T> R = make_rot(C, s, c);
+      T Vn[6], Vdn[6];
+      fwd_step<T, true>(C, R, C.pm[0], C.pm[1], C.pm[2], c_qd, c_qa, V, Vd, Vn, Vdn);
+      T st[8];
+      st[0] = s;
+      st[1] = c;
+      bias_force(C, Vn, Vdn, st + 2);
+      if (i < lt) {
+        TmemIO<T>::st(tbase + (uint32_t)(i * TmemIO<T>::kCols), st);
+      } else {
+        T* d = sstash + (size_t)(i - lt) * 8 * NT + tid;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) d[k * NT] = st[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 6; ++k) { V[k] = Vn[k]; Vd[k] = Vdn[k]; }
+      c_q = n_q; c_qd = n_qd; c_qa = n_qa;
+      n_q = f_q; n_qd = f_qd; n_qa = f_qa;
+    }
+    tmem_wait_st();
+
+    // ---------------- backward sweep, Eq. (2):
+    // F_n = Fhat_n + F_{n+1}, F_i = Fhat_i + Ad^T_{f_{i,i+1}^{-1}} F_{i+1}, tau_i = F_i[5] (joint frame).
+    T F[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) F[k] = P.bnd.Ftip[k];
+    Rot<T> Rn;
+    T pn0 = 0, pn1 = 0, pn2 = 0;
+    bool tip = true;
+    T* tcol = tau + b;
+    // (a) links in shared memory, i = n-1 .. lt
+    for (int i = n - 1; i >= lt; --i) {
+      const T* d = sstash + (size_t)(i - lt) * 8 * NT + tid;
+      T cur[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cur[k] = d[k * NT];
+      if (tip) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) F[k] += cur[2 + k];
+        tip = false;
+      } else {
+        T Fo[6];
+        bwd_step(Rn, pn0, pn1, pn2, F, cur + 2, Fo);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) F[k] = Fo[k];
+      }
+      if (valid) tcol[(int64_t)i * B] = F[5];
+      const LinkConst<T>& C = P.L[i];
+      Rn = make_rot(C, cur[0], cur[1]);
+      pn0 = C.pm[0]; pn1 = C.pm[1]; pn2 = C.pm[2];
+    }
+    // (b) links in TMEM, i = lt-1 .. 0, with the next link's tcgen05.ld in flight
+    typename TmemIO<T>::Regs rA;
+    if (lt > 0) TmemIO<T>::ld(tbase + (uint32_t)((lt - 1) * TmemIO<T>::kCols), rA);
+    for (int i = lt - 1; i >= 0; --i) {
+      TmemIO<T>::wait(rA);
+      T cur[8];
+      TmemIO<T>::unpack(rA, cur);
+      if (i > 0) TmemIO<T>::ld(tbase + (uint32_t)((i - 1) * TmemIO<T>::kCols), rA);
+      if (tip) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) F[k] += cur[2 + k];
+        tip = false;
+      } else {
+        T Fo[6];
+        bwd_step(Rn, pn0, pn1, pn2, F, cur + 2, Fo);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) F[k] = Fo[k];
+      }
+      if (valid) tcol[(int64_t)i * B] = F[5];
+      const LinkConst<T>& C = P.L[i];
+      Rn = make_rot(C, cur[0], cur[1]);
+      pn0 = C.pm[0]; pn1 = C.pm[1]; pn2 = C.pm[2];
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (warp == 0) tmem_dealloc_512(tmem_slot);
+}
+
+// ------------------------------------------------------------------ ping-pong kernel
+// Same arithmetic, but the backward sweep of tile t-1 and the forward sweep of
+// tile t run in the SAME loop (step k: backward of link n-1-k, forward of link
+// k): two independent dependency chains per thread, i.e. twice the ILP, at no
+// extra stash.  Tile parity alternates the link->slot map (slot(j) = j for even
+// tiles, n-1-j for odd ones) so that at step k both sweeps touch the same slot:
+// the backward read of the old tile's link frees exactly the slot the forward
+// write of the new tile needs.  Every steady-state
+// step is ONE basic block (no branch between the two sweeps), so ptxas can
+// interleave them; the slot kind (TMEM or shared) is fixed per loop segment.
+template <typename T>
+struct FwdState {
+  T V[6], Vd[6];
+  T c_q, c_qd, c_qa, n_q, n_qd, n_qa;
+  const T *pq, *pqd, *pqa;
+};
+template <typename T>
+struct BwdState {
+  T F[6];
+  Rot<T> Rn;
+  T pn0, pn1, pn2;
+  int64_t b;
+  bool valid;
+};
+
+template <typename T>
+__device__ __forceinline__ void fwd_init(FwdState<T>& f, const ThreadParams<T>& P, int64_t B, int64_t bl,
+                                         const T* q, const T* qd, const T* qdd) {
+#pragma unroll
+  for (int k = 0; k < 6; ++k) { f.V[k] = P.bnd.V0[k]; f.Vd[k] = P.bnd.Vd0[k]; }
+  f.pq = q + bl; f.pqd = qd + bl; f.pqa = qdd + bl;
+  f.c_q = __ldg(f.pq); f.c_qd = __ldg(f.pqd); f.c_qa = __ldg(f.pqa);
+  const int64_t off1 = (int64_t)(P.n > 1 ? 1 : 0) * B;
+  f.n_q = __ldg(f.pq + off1); f.n_qd = __ldg(f.pqd + off1); f.n_qa = __ldg(f.pqa + off1);
+}
+template <typename T>
+__device__ __forceinline__ void bwd_init(BwdState<T>& g, const ThreadParams<T>& P) {
+#pragma unroll
+  for (int k = 0; k < 6; ++k) g.F[k] = P.bnd.Ftip[k];
+  g.Rn = Rot<T>{1, 0, 0, 0, 1, 0, 0, 0, 1};     // f_{n,n+1} = I (A5)
+  g.pn0 = g.pn1 = g.pn2 = 0;
+}
+// forward link k: V_k, Vdot_k, Fhat_k -> st[8]
+template <typename T>
+__device__ __forceinline__ void fwd_link(FwdState<T>& f, const ThreadParams<T>& P, int64_t B, int k, T* st) {
+  const int n = P.n;
+  const int64_t off2 = (int64_t)min(k + 2, n - 1) * B;
+  const T f_q = __ldg(f.pq + off2), f_qd = __ldg(f.pqd + off2), f_qa = __ldg(f.pqa + off2);
+  const LinkConst<T>& C = P.L[k];
+  T s, c;
+  rd_sincos(f.c_q, &s, &c);
+  const Rot<T> R = make_rot(C, s, c);
+  T Vn[6], Vdn[6];
+  fwd_step<T, true>(C, R, C.pm[0], C.pm[1], C.pm[2], f.c_qd, f.c_qa, f.V, f.Vd, Vn, Vdn);
+  st[0] = s;
+  st[1] = c;
+  bias_force(C, Vn, Vdn, st + 2);
+#pragma unroll
+  for (int j = 0; j < 6; ++j) { f.V[j] = Vn[j]; f.Vd[j] = Vdn[j]; }
+  f.c_q = f.n_q; f.c_qd = f.n_qd; f.c_qa = f.n_qa;
+  f.n_q = f_q; f.n_qd = f_qd; f.n_qa = f_qa;
+}
+// backward link i from its stash cur[8]: F_i, tau_i, then (R, p) of link i for link i-1
+template <typename T>
+__device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& P, int64_t B, int i,
+                                         const T* cur, T* __restrict__ tau) {
+  T Fo[6];
+  bwd_step(g.Rn, g.pn0, g.pn1, g.pn2, g.F, cur + 2, Fo);
+#pragma unroll
+  for (int j = 0; j < 6; ++j) g.F[j] = Fo[j];
+  if (g.valid) tau[(int64_t)i * B + g.b] = g.F[5];
+  const LinkConst<T>& C = P.L[i];
+  g.Rn = make_rot(C, cur[0], cur[1]);
+  g.pn0 = C.pm[0]; g.pn1 = C.pm[1]; g.pn2 = C.pm[2];
+}
+
+template <typename T, int W>
+__global__ void __launch_bounds__(W * 32, 1)
+rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
+                      const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
+                      T* __restrict__ tau) {
+  constexpr int NT = W * 32;
+  constexpr int kColsPerWarp = 2048 / W;
+  constexpr int KC = TmemIO<T>::kCols;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sstash = reinterpret_cast<T*>(smem_raw);     // slots lt..n-1: [slot - lt][8][NT]
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5;
+  const int tid = threadIdx.x;
+  if (warp == 0) tmem_alloc_512(&tmem_slot);
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tbase = tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * kColsPerWarp);
+  const int n = P.n, lt = P.lt;
+  const int64_t ntiles = (B + NT - 1) / NT;
+  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto sptr = [&](int slot) { return sstash + (size_t)(slot - lt) * 8 * NT + tid; };
+  auto put_smem = [&](int slot, const T* st) {
+    T* d = sptr(slot);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) d[k * NT] = st[k];
+  };
+  auto get_smem = [&](int slot, T* cur) {
+    const T* d = sptr(slot);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cur[k] = d[k * NT];
+  };
+  auto put_any = [&](int slot, const T* st) {
+    if (slot < lt) TmemIO<T>::st(tbase + (uint32_t)(slot * KC), st);
+    else put_smem(slot, st);
+  };
+  auto get_any = [&](int slot, T* cur) {
+    if (slot < lt) {
+      typename TmemIO<T>::Regs r;
+      TmemIO<T>::ld(tbase + (uint32_t)(slot * KC), r);
+      TmemIO<T>::wait(r);
+      TmemIO<T>::unpack(r, cur);
+    } else {
+      get_smem(slot, cur);
+    }
+  };
+
+  FwdState<T> f;
+  BwdState<T> g;
+  g.b = 0;
+  g.valid = false;
+  for (int64_t it = 0; it <= my_tiles; ++it) {
+    const int64_t b = (blockIdx.x + it * gridDim.x) * NT + tid;
+    const bool fvalid = b < B;
+    if (it == my_tiles) {
+      if (it == 0) break;
+      // epilogue: backward of the last tile alone (slot parity of tile it-1)
+      const int bpar = (int)((it - 1) & 1);
+      bwd_init(g, P);
+      for (int i = n - 1; i >= 0; --i) {
+        T cur[8];
+        get_any(bpar ? n - 1 - i : i, cur);
+        bwd_link(g, P, B, i, cur, tau);
+      }
+      break;
+    }
+    fwd_init(f, P, B, fvalid ? b : (B - 1), q, qd, qdd);
+    if (it == 0) {
+      // prologue: forward of the first tile alone (parity 0: slot = link)
+      for (int k = 0; k < n; ++k) {
+        T st[8];
+        fwd_link(f, P, B, k, st);
+        put_any(k, st);
+      }
+    } else {
+      // steady state: backward of tile it-1 (parity bpar) + forward of tile it (parity !bpar);
+      // at step k both use slot s_k = bpar ? k : n-1-k.
+      bwd_init(g, P);
+      const int bpar = (int)((it - 1) & 1);
+      auto smem_step = [&](int k) {
+        const int slot = bpar ? k : n - 1 - k;
+        T cur[8], st[8];
+        get_smem(slot, cur);
+        bwd_link(g, P, B, n - 1 - k, cur, tau);
+        fwd_link(f, P, B, k, st);
+        put_smem(slot, st);
+      };
+      auto tmem_seg = [&](int k0, int k1) {
+        if (k0 >= k1) return;
+        typename TmemIO<T>::Regs r;
+        TmemIO<T>::ld(tbase + (uint32_t)((bpar ? k0 : n - 1 - k0) * KC), r);
+        for (int k = k0; k < k1; ++k) {
+          const int slot = bpar ? k : n - 1 - k;
+          const int knx = min(k + 1, k1 - 1);
+          const int slot_nx = bpar ? knx : n - 1 - knx;
+          TmemIO<T>::wait(r);
+          T cur[8], st[8];
+          TmemIO<T>::unpack(r, cur);
+          TmemIO<T>::ld(tbase + (uint32_t)(slot_nx * KC), r);       // next step's slot, in flight
+          bwd_link(g, P, B, n - 1 - k, cur, tau);
+          fwd_link(f, P, B, k, st);
+          TmemIO<T>::st(tbase + (uint32_t)(slot * KC), st);
+        }
+        TmemIO<T>::wait(r);
+      };
+      if (bpar) {
+        tmem_seg(0, lt);
+        for (int k = lt; k < n; ++k) smem_step(k);
+      } else {
+        for (int k = 0; k < n - lt; ++k) smem_step(k);
+        tmem_seg(n - lt, n);
+      }
+    }
+    tmem_wait_st();
+    g.b = b;
+    g.valid = fvalid;
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -234,57 +443,71 @@ int num_sms() {
   return sms;
 }
 
-// Stash selection: RD_STASH=local|tmem (default tmem) -- an experiment knob
-// read once; the default is the measured winner.
-static int stash_choice() {
-  static int c = -1;
-  if (c < 0) {
-    const char* e = getenv("RD_STASH");
-    c = (e && e[0] == 'l') ? kLocal : kTmem;
+// Stash plan: the largest W in {16, 8} whose TMEM + shared-memory capacity
+// holds n links.
+struct StashPlan { int W, lt, ls; size_t smem; };
+static constexpr size_t kSmemCap = 227 * 1024;
+static constexpr size_t kSmemFloor = 120 * 1024;   // forces one CTA per SM (it owns all TMEM)
+
+template <typename T>
+static bool plan_for(int n, StashPlan* out) {
+  for (int W : {16, 8}) {
+    const int cols_per_warp = 2048 / W;
+    const int lt_cap = cols_per_warp / TmemIO<T>::kCols;
+    const int lt = n < lt_cap ? n : lt_cap;
+    const int ls = n - lt;
+    const size_t smem = (size_t)ls * 8 * sizeof(T) * W * 32;
+    if (smem <= kSmemCap - 1024) {
+      out->W = W; out->lt = lt; out->ls = ls;
+      out->smem = smem < kSmemFloor ? kSmemFloor : smem;
+      return true;
+    }
   }
-  return c;
-}
-
-template <typename T, int N>
-static cudaError_t launch_n(const LinkConst<T>* Lh, const Boundary<T>& bnd, int64_t B, const T* q,
-                            const T* qd, const T* qdd, T* tau, cudaStream_t st, int* launches) {
-  RneaParams<T, N> P;
-  for (int i = 0; i < N; ++i) P.L[i] = Lh[i];
-  P.bnd = bnd;
-  const int64_t ntiles = (B + 127) / 128;
-  if (stash_choice() == kTmem) {
-    const int64_t grid = ntiles < num_sms() ? ntiles : num_sms();
-    rnea_thread_tmem_kernel<T, N><<<(unsigned)grid, 128, 0, st>>>(P, B, q, qd, qdd, tau);
-  } else {
-    rnea_thread_local_kernel<T, N><<<(unsigned)ntiles, 128, 0, st>>>(P, B, q, qd, qdd, tau);
-  }
-  ++*launches;
-  return cudaGetLastError();
-}
-
-// Compile-time link counts with a specialised kernel (others use rnea_generic).
-#define RD_THREAD_NS(X) X(1) X(2) X(3) X(6) X(7) X(10) X(30)
-
-bool thread_kernel_has_n(int n, bool) {
-#define RD_CASE(K) if (n == K) return true;
-  RD_THREAD_NS(RD_CASE)
-#undef RD_CASE
   return false;
+}
+
+bool thread_kernel_has_n(int n, bool fp64) {
+  if (n < 1 || n > kMaxThreadN) return false;
+  StashPlan p;
+  return fp64 ? plan_for<double>(n, &p) : plan_for<float>(n, &p);
+}
+
+template <typename T, int W, bool PP>
+static cudaError_t launch_w(const ThreadParams<T>& P, size_t smem, int64_t B, const T* q, const T* qd,
+                            const T* qdd, T* tau, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(PP ? (const void*)rnea_thread_pp_kernel<T, W> : (const void*)rnea_thread_kernel<T, W>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kSmemCap - 1024));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t ntiles = (B + W * 32 - 1) / (W * 32);
+  const int64_t grid = ntiles < num_sms() ? ntiles : num_sms();
+  if (PP) rnea_thread_pp_kernel<T, W><<<(unsigned)grid, W * 32, smem, st>>>(P, B, q, qd, qdd, tau);
+  else rnea_thread_kernel<T, W><<<(unsigned)grid, W * 32, smem, st>>>(P, B, q, qd, qdd, tau);
+  return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_rnea_thread(int n, const LinkConst<T>* L_host, const Boundary<T>& bnd, int64_t B,
                                const T* q, const T* qd, const T* qdd, T* tau, cudaStream_t st,
                                int* launches, bool* supported) {
-  *supported = true;
-  switch (n) {
-#define RD_CASE(K) case K: return launch_n<T, K>(L_host, bnd, B, q, qd, qdd, tau, st, launches);
-    RD_THREAD_NS(RD_CASE)
-#undef RD_CASE
-    default:
-      *supported = false;
-      return cudaSuccess;
-  }
+  StashPlan plan;
+  *supported = n >= 1 && n <= kMaxThreadN && plan_for<T>(n, &plan);
+  if (!*supported) return cudaSuccess;
+  ThreadParams<T> P;
+  for (int i = 0; i < n; ++i) P.L[i] = L_host[i];
+  P.bnd = bnd;
+  P.n = n;
+  P.lt = plan.lt;
+  ++*launches;
+  static const bool pipe = !(getenv("RD_PP") && getenv("RD_PP")[0] == '0');   // ping-pong default
+  if (plan.W == 16) return pipe ? launch_w<T, 16, true>(P, plan.smem, B, q, qd, qdd, tau, st)
+                                : launch_w<T, 16, false>(P, plan.smem, B, q, qd, qdd, tau, st);
+  return pipe ? launch_w<T, 8, true>(P, plan.smem, B, q, qd, qdd, tau, st)
+              : launch_w<T, 8, false>(P, plan.smem, B, q, qd, qdd, tau, st);
 }
 
 template cudaError_t launch_rnea_thread<double>(int, const LinkConst<double>*, const Boundary<double>&, int64_t,

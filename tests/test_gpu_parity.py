@@ -258,3 +258,24 @@ def test_fd_tip_wrench(rd):
     tau = np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b], None, Vd0, Ft) for b in range(200)], 1)
     out = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()
     assert rel_err_per_state(out, qdd, floor=1.0).max() < 1e-9
+
+
+@pytest.mark.parametrize("dtype,scale", [(torch.float64, 1e4), (torch.float32, 1e3)])
+def test_large_joint_angles(rd, dtype, scale):
+    # the branch-free sin/cos reduction (rd_math.cuh) against the oracle's libm.
+    # (At |q| ~ 1e6 the ORACLE's own Rodrigues translation, (I q + ... + (q - s)[w]^2) v,
+    # cancels O(|q|) terms and loses ~1e-10 relative accuracy, so 1e4 is the largest
+    # scale at which the oracle is a 1e-10 reference.)
+    r = synth.random_chain(30, 1030)
+    q, qd, qdd = synth.states(21, 30, 0, 5000)
+    q = q / np.pi * scale
+    for strat in ("thread", "generic"):
+        check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype, strategy=strat)
+
+
+def test_thread_kernel_many_tiles(rd):
+    # many tiles per CTA: exercises the ping-pong slot parity over > 2 tiles per CTA
+    cfg = synth.CONFIGS["C3"]
+    q, qd, qdd = synth.states(cfg["seed"], 30, 0, 70000)
+    check_id(rd, synth.robot_for(cfg), cfg["gravity"], q, qd, qdd, strategy="thread",
+             sample=np.arange(0, 70000, 7))

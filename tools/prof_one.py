@@ -1,0 +1,30 @@
+"""Run one config/strategy a few times (for ncu captures)."""
+import argparse, os, sys
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth
+import paper_1609_04493_b200 as rd
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C3")
+ap.add_argument("--strategy", default="auto")
+ap.add_argument("--dtype", default="f64")
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--batch", type=int, default=0)
+ap.add_argument("--fd", action="store_true")
+a = ap.parse_args()
+cfg = synth.CONFIGS[a.config]
+n = cfg["n"]; B = a.batch or cfg["batch"]
+dt = torch.float64 if a.dtype == "f64" else torch.float32
+q, qd, qdd = synth.states(cfg["seed"], n, 0, B, cfg["ranges"])
+tq, tqd, tqdd = (torch.from_numpy(x).to("cuda", dt) for x in (q, qd, qdd))
+m = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
+m.set_strategy(a.strategy)
+out = torch.empty_like(tq)
+for _ in range(a.reps):
+    if a.fd:
+        rd.forward_dynamics(m, tq, tqd, tqdd, out)
+    else:
+        rd.inverse_dynamics(m, tq, tqd, tqdd, out)
+torch.cuda.synchronize()
+print("done", a)
