@@ -146,7 +146,14 @@ def run_reference(args):
     robot = synth.robot_for(cfg)
     g = cfg["gravity"]
     cores = os.cpu_count() or 1
-    sample = args.ref_sample
+    # bounded sample per step: calibrate the oracle's rate, then size each step so the
+    # whole --warmup + --steps run takes about --ref-seconds (capped at --ref-sample states)
+    cal = 2048
+    qc, qdc, qddc = synth.states(cfg["seed"], n, 0, cal, cfg["ranges"])
+    t0 = time.perf_counter()
+    oracle.rnea_batch(robot, g, qc, qdc, qddc, nthreads=cores)
+    rate = cal / max(time.perf_counter() - t0, 1e-6)
+    sample = int(min(args.ref_sample, max(1024, rate * args.ref_seconds / (args.steps + args.warmup))))
     q, qd, qdd = synth.states(cfg["seed"], n, 0, sample, cfg["ranges"])
     for _ in range(args.warmup):
         oracle.rnea_batch(robot, g, q, qd, qdd, nthreads=cores)
@@ -184,6 +191,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=65536)
+    ap.add_argument("--ref-seconds", type=float, default=60.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
