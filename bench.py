@@ -113,7 +113,7 @@ def cpu_baseline(robot, g, cfg, n, seconds=10.0):
     chunk = 4096 * cores // 8 if cores >= 8 else 4096
     done, t_total, b0 = 0, 0.0, 0
     oracle.rnea_batch(robot, g, *synth.states(cfg["seed"], n, 0, 64, cfg["ranges"]), nthreads=cores)
-    while t_total < seconds and done < 4_000_000:
+    while t_total < seconds and done < 40_000_000:
         q, qd, qdd = synth.states(cfg["seed"], n, b0, b0 + chunk, cfg["ranges"])
         t0 = time.perf_counter()
         oracle.rnea_batch(robot, g, q, qd, qdd, nthreads=cores)
@@ -123,6 +123,25 @@ def cpu_baseline(robot, g, cfg, n, seconds=10.0):
     return {"value": done / t_total, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"first {done} states of the {cfg['name']} workload (n={n}), oracle::rnea "
                       f"(C++ -O2, dense 6x6 Eq. 1-2) on {cores} host threads, {t_total:.1f} s"}
+
+
+def cpu_baseline_fd(robot, g, cfg, n, seconds=10.0):
+    """The oracle's ABA (Eq. 7-8) on all host cores, on a bounded sample of the FD workload."""
+    import oracle
+    cores = os.cpu_count() or 1
+    chunk = 512 * max(1, cores // 4)
+    done, t_total, b0 = 0, 0.0, 0
+    while t_total < seconds and done < 2_000_000:
+        q, qd, qdd = synth.states(cfg["seed"], n, b0, b0 + chunk, cfg["ranges"])
+        tau = oracle.rnea_batch(robot, g, q, qd, qdd, nthreads=cores)
+        t0 = time.perf_counter()
+        oracle.fd_batch(robot, g, q, qd, tau, nthreads=cores)
+        t_total += time.perf_counter() - t0
+        done += chunk
+        b0 += chunk
+    return {"value": done / t_total, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {done} states of the {cfg['name']} FD workload (n={n}), oracle::fd_aba "
+                      f"(C++ -O2, Eq. 7-8) on {cores} host threads, {t_total:.1f} s"}
 
 
 def load_traffic(cfg_name: str, dtype: str):
@@ -148,18 +167,26 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     # bounded sample per step: calibrate the oracle's rate, then size each step so the
     # whole --warmup + --steps run takes about --ref-seconds (capped at --ref-sample states)
-    cal = 2048
+    fd = args.config == "C4"
+    cal = 256 if fd else 2048
     qc, qdc, qddc = synth.states(cfg["seed"], n, 0, cal, cfg["ranges"])
+    if fd:
+        tc = oracle.rnea_batch(robot, g, qc, qdc, qddc, nthreads=cores)
+        run = lambda a, b, c, t: oracle.fd_batch(robot, g, a, b, t, nthreads=cores)  # noqa: E731
+    else:
+        tc = None
+        run = lambda a, b, c, t: oracle.rnea_batch(robot, g, a, b, c, nthreads=cores)  # noqa: E731
     t0 = time.perf_counter()
-    oracle.rnea_batch(robot, g, qc, qdc, qddc, nthreads=cores)
+    run(qc, qdc, qddc, tc)
     rate = cal / max(time.perf_counter() - t0, 1e-6)
-    sample = int(min(args.ref_sample, max(1024, rate * args.ref_seconds / (args.steps + args.warmup))))
+    sample = int(min(args.ref_sample, max(256, rate * args.ref_seconds / (args.steps + args.warmup))))
     q, qd, qdd = synth.states(cfg["seed"], n, 0, sample, cfg["ranges"])
+    tq = oracle.rnea_batch(robot, g, q, qd, qdd, nthreads=cores) if fd else None
     for _ in range(args.warmup):
-        oracle.rnea_batch(robot, g, q, qd, qdd, nthreads=cores)
+        run(q, qd, qdd, tq)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.rnea_batch(robot, g, q, qd, qdd, nthreads=cores)
+        run(q, qd, qdd, tq)
     dt = time.perf_counter() - t0
     value = sample * args.steps / dt
     line = {
@@ -167,10 +194,12 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{args.config}: n={n} random chain RNEA (bounded sample of {sample} states/step)",
+        "config": {"workload": f"{args.config}: n={n} {'FD (ABA)' if fd else 'RNEA'} (bounded sample of {sample} "
+                               f"states/step of the workload)",
                    "n": n, "states_per_step": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"{sample} states of {args.config} per step, oracle::rnea on {cores} threads"},
+                         "sample": f"{sample} states of {args.config} per step, oracle::"
+                                   f"{'fd_aba' if fd else 'rnea'} on {cores} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -188,6 +217,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="states per GPU (default: the config's)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--gather", action="store_true", help="time a final all-gather of tau (off the hot path)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=65536)
@@ -210,12 +240,11 @@ def main():
     cfg = dict(synth.CONFIGS[args.config], name=args.config)
     n = cfg["n"]
     fd = args.config == "C4"
+    from paper_1609_04493_b200.sharding import shard_range, gather_rows
     per_gpu = args.batch or cfg["batch"]
-    if args.scaling == "strong":
-        total = per_gpu
-        per_gpu = (total + world - 1) // world
-    b0 = rank * per_gpu
-    b1 = b0 + per_gpu
+    total = per_gpu * world if args.scaling == "weak" else per_gpu
+    b0, b1 = shard_range(total, world, rank)       # contiguous global-index shard
+    per_gpu = b1 - b0
     robot = synth.robot_for(cfg)
     g = cfg["gravity"]
     dt = torch.float64 if args.dtype == "f64" else torch.float32
@@ -272,8 +301,19 @@ def main():
         tt = torch.tensor([total_ms, avg_kernel_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms, avg_kernel_ms = float(tt[0]), float(tt[1])
-    units = per_gpu * world * args.steps
+    units = total * args.steps
     value = units / (total_ms / 1e3)
+
+    # optional final gather of tau to every rank over NCCL, timed separately
+    gather_ms = None
+    if args.gather and world > 1:
+        import torch.distributed as dist
+        barrier()
+        g0 = time.perf_counter()
+        full = gather_rows(out, total)
+        torch.cuda.synchronize()
+        gather_ms = (time.perf_counter() - g0) * 1e3
+        del full
 
     # e2e: through the public host-buffer API (pinned host arrays, H2D + kernel + D2H per step)
     e2e = None
@@ -291,8 +331,8 @@ def main():
             tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_s = float(tt[0])
-        e2e = {"value": per_gpu * world * args.e2e_steps / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": 3 * n * per_gpu * 8 * world, "d2h_bytes_per_step": n * per_gpu * 8 * world,
+        e2e = {"value": total * args.e2e_steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": 3 * n * total * 8, "d2h_bytes_per_step": n * total * 8,
                "api": "rd_inverse_dynamics_host_f64 (pinned host buffers, chunked 2-stream pipeline)"}
 
     if rank != 0:
@@ -313,7 +353,7 @@ def main():
         "config": {"workload": f"{args.config}: {'FD (ABA)' if fd else 'RNEA'} n={n} random serial chain, "
                                f"{per_gpu} states per GPU" if cfg['robot'] == 'random' else
                                f"{args.config}: {cfg['robot']} n={n}, {per_gpu} states per GPU",
-                   "n": n, "states_per_gpu": per_gpu, "global_batch": per_gpu * world,
+                   "n": n, "states_per_gpu": per_gpu, "global_batch": total, "gather_ms": gather_ms,
                    "parallelism": f"batch-sharded x{world} (no collective on the hot path)",
                    "strategy": strat, "robot_seed": 1000 + n if cfg["robot"] == "random" else cfg["robot"],
                    "state_seed": cfg["seed"], "l2": l2_note},
@@ -329,7 +369,9 @@ def main():
         "gpu_launches": launches,
         "e2e": e2e,
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and fd:
+        line["cpu_baseline"] = cpu_baseline_fd(robot, g, cfg, n, args.cpu_seconds)
+    elif not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(robot, g, cfg, n, args.cpu_seconds)
     print(json.dumps(line), flush=True)
     if world > 1:

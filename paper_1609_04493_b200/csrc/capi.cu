@@ -235,12 +235,22 @@ template <typename T> const rd::Boundary<T>& bnd(rd_model_t m);
 template <> const rd::Boundary<double>& bnd<double>(rd_model_t m) { return m->b64; }
 template <> const rd::Boundary<float>& bnd<float>(rd_model_t m) { return m->b32; }
 
+// Strategy table (measured on B200, profiles/r01):
+//  * batch <= kWarpScanMaxBatch and n <= 32 -> WARP_SCAN: one warp per state,
+//    lane = link, log-depth shuffle scans; the latency regime (paper P:505/P:524),
+//    e.g. n = 30, B = 1..1000: 21-24 us vs 43-49 us for THREAD;
+//  * otherwise THREAD when the on-chip stash fits (n <= 30 fp64 / 32 fp32, all
+//    joints revolute with zero pitch): 3.9x faster than WARP_SCAN at B = 1M;
+//  * otherwise GENERIC (any n, any joint type).
+constexpr int64_t kWarpScanMaxBatch = 4096;
+
 rd_strategy_t resolve(rd_model_t m, int64_t batch, bool fp64) {
-  (void)batch;
   if (m->strategy == RD_STRAT_GENERIC) return RD_STRAT_GENERIC;
   const bool thread_ok = m->all_revolute && rd::thread_kernel_has_n(m->n, fp64);
+  const bool warp_ok = m->n <= 32;
   if (m->strategy == RD_STRAT_THREAD) return thread_ok ? RD_STRAT_THREAD : RD_STRAT_GENERIC;
-  if (m->strategy == RD_STRAT_WARP_SCAN) return RD_STRAT_WARP_SCAN;
+  if (m->strategy == RD_STRAT_WARP_SCAN) return warp_ok ? RD_STRAT_WARP_SCAN : RD_STRAT_GENERIC;
+  if (warp_ok && batch <= kWarpScanMaxBatch) return RD_STRAT_WARP_SCAN;
   return thread_ok ? RD_STRAT_THREAD : RD_STRAT_GENERIC;
 }
 
@@ -260,7 +270,7 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   } else if (strat == RD_STRAT_WARP_SCAN) {
     bool ok = false;
     e = rd::launch_rnea_warp<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok);
-    if (!ok) return fail(RD_E_UNSUPPORTED, "warp-scan strategy supports n <= 32 only");
+    if (!ok) strat = RD_STRAT_GENERIC;
   }
   if (strat == RD_STRAT_GENERIC) {
     std::lock_guard<std::mutex> lk(m->mu);

@@ -55,7 +55,7 @@ def check_id(rd, robot, g, q, qd, qdd, dtype=torch.float64, strategy="auto", sam
 def test_C1_planar2_closed_form_config(rd):
     cfg = synth.CONFIGS["C1"]
     q, qd, qdd = synth.states(cfg["seed"], 2, 0, cfg["batch"], cfg["ranges"])
-    for strat in ("auto", "thread", "generic"):
+    for strat in ("auto", "thread", "generic", "warp_scan"):
         check_id(rd, synth.planar2(), cfg["gravity"], q, qd, qdd, strategy=strat)
 
 
@@ -63,7 +63,7 @@ def test_C1_planar2_closed_form_config(rd):
 def test_C2_arm7(rd, dtype):
     cfg = synth.CONFIGS["C2"]
     q, qd, qdd = synth.states(cfg["seed"], 7, 0, cfg["batch"], cfg["ranges"])
-    for strat in ("thread", "generic"):
+    for strat in ("thread", "generic", "warp_scan"):
         check_id(rd, synth.arm7(), cfg["gravity"], q, qd, qdd, dtype, strategy=strat)
 
 
@@ -80,7 +80,7 @@ def test_C3_full_size_sampled(rd, dtype):
     check_id(rd, synth.robot_for(cfg), cfg["gravity"], q, qd, qdd, dtype, sample=sample)
 
 
-@pytest.mark.parametrize("strategy", ["thread", "generic"])
+@pytest.mark.parametrize("strategy", ["thread", "generic", "warp_scan"])
 def test_C3_small_all_states(rd, strategy):
     cfg = synth.CONFIGS["C3"]
     q, qd, qdd = synth.states(cfg["seed"], 30, 0, 3000, cfg["ranges"])
@@ -92,7 +92,8 @@ def test_C3_small_all_states(rd, strategy):
 def test_ragged_batches(rd, B):
     r = synth.random_chain(30, 1030)
     q, qd, qdd = synth.states(7, 30, 0, B)
-    check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd)
+    for strat in ("auto", "thread", "warp_scan", "generic"):
+        check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strat)
 
 
 def test_empty_batch_is_noop(rd):
@@ -105,7 +106,7 @@ def test_empty_batch_is_noop(rd):
 def test_link_counts_random_chains(rd, n):
     r = synth.random_chain(n, 500 + n)
     q, qd, qdd = synth.states(11, n, 0, 777)
-    for strat in ("auto", "generic"):
+    for strat in ("auto", "generic") + (("warp_scan",) if n <= 32 else ()):
         check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strat)
 
 
@@ -118,7 +119,8 @@ def test_prismatic_and_screw_joints_generic(rd, dtype):
             r["S"][i, :3] += 0.2 * r["S"][i, 3:]
             break
     q, qd, qdd = synth.states(12, 12, 0, 2000)
-    check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype)
+    for strat in ("generic", "warp_scan"):
+        check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype, strategy=strat)
 
 
 def test_pendulum_closed_form_on_gpu(rd):
@@ -138,7 +140,7 @@ def test_full_boundary_V0_Vdot0_Ftip(rd):
     model = rd.Model.from_robot(r, (0, 0, 0))
     model.set_boundary(V0, Vd0, Ft)
     q, qd, qdd = synth.states(13, 7, 0, 300)
-    for strat in ("generic",):
+    for strat in ("generic", "warp_scan"):
         model.set_strategy(strat)
         tau = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd)).cpu().numpy()
         ref = np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b], V0, Vd0, Ft) for b in range(300)], 1)
@@ -146,7 +148,7 @@ def test_full_boundary_V0_Vdot0_Ftip(rd):
     r2 = synth.random_chain(7, 32)                 # all revolute -> thread kernel
     model2 = rd.Model.from_robot(r2, (0, 0, 0))
     model2.set_boundary(V0, Vd0, Ft)
-    for strat in ("thread", "generic"):
+    for strat in ("thread", "generic", "warp_scan"):
         model2.set_strategy(strat)
         tau = rd.inverse_dynamics(model2, dev(q), dev(qd), dev(qdd)).cpu().numpy()
         ref = np.stack([oracle.rnea(r2, q[:, b], qd[:, b], qdd[:, b], V0, Vd0, Ft) for b in range(300)], 1)
@@ -157,12 +159,15 @@ def test_deterministic_and_strategy_consistent(rd):
     cfg = synth.CONFIGS["C3"]
     q, qd, qdd = synth.states(cfg["seed"], 30, 0, 20000)
     model = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
-    a = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd))
-    b = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd))
-    assert torch.equal(a, b)                       # bit-identical repeat
-    # a shard evaluated alone equals the same states inside the full batch
-    c = rd.inverse_dynamics(model, dev(q[:, 5000:9000]), dev(qd[:, 5000:9000]), dev(qdd[:, 5000:9000]))
-    assert torch.equal(a[:, 5000:9000], c)
+    for strat in ("thread", "warp_scan", "generic"):
+        # with a FIXED strategy, results are bit-identical across repeats and across sharding
+        # (AUTO picks the strategy from the per-call batch size)
+        model.set_strategy(strat)
+        a = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd))
+        b = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd))
+        assert torch.equal(a, b)                       # bit-identical repeat
+        c = rd.inverse_dynamics(model, dev(q[:, 5000:9000]), dev(qd[:, 5000:9000]), dev(qdd[:, 5000:9000]))
+        assert torch.equal(a[:, 5000:9000], c)
 
 
 def test_host_path_equals_device_path(rd):
@@ -269,7 +274,7 @@ def test_large_joint_angles(rd, dtype, scale):
     r = synth.random_chain(30, 1030)
     q, qd, qdd = synth.states(21, 30, 0, 5000)
     q = q / np.pi * scale
-    for strat in ("thread", "generic"):
+    for strat in ("thread", "generic", "warp_scan"):
         check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype, strategy=strat)
 
 

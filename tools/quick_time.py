@@ -35,12 +35,24 @@ def main():
         tq, tqd, tqdd = (torch.from_numpy(x).to("cuda", dt) for x in (q, qd, qdd))
         model = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
         out = torch.empty_like(tq)
-        for strat in ("thread", "generic"):
+        for strat in ("thread", "generic", "warp_scan"):
             model.set_strategy(strat)
             ms = time_call(lambda: rd.inverse_dynamics(model, tq, tqd, tqdd, out))
             flops = (379 * n - 96) * B
             print(f"{name} {str(dt)[6:]} {strat:8s} n={n} B={B}: {ms:.4f} ms  {B / ms * 1e3:.3e} evals/s  "
                   f"{flops / ms / 1e9:.2f} TFLOP/s (lean)", flush=True)
+    # small-batch latency sweep (paper's group-number axis)
+    cfg = synth.CONFIGS["C3"]
+    model = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
+    for B in (1, 32, 1000, 10000, 100000):
+        q, qd, qdd = synth.states(cfg["seed"], 30, 0, B)
+        tq, tqd, tqdd = (torch.from_numpy(x).cuda() for x in (q, qd, qdd))
+        out = torch.empty_like(tq)
+        res = []
+        for strat in ("thread", "warp_scan", "generic"):
+            model.set_strategy(strat)
+            res.append(f"{strat}={time_call(lambda: rd.inverse_dynamics(model, tq, tqd, tqdd, out)) * 1e3:.1f}us")
+        print(f"C3-robot B={B}: " + " ".join(res), flush=True)
     cfg = synth.CONFIGS["C4"]
     n, B = cfg["n"], cfg["batch"]
     q, qd, qdd = synth.states(cfg["seed"], n, 0, B)
