@@ -3,6 +3,7 @@
 // (end-to-end) pipeline.  No torch types, no exceptions across the ABI.
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -140,6 +141,12 @@ struct rd_model_s {
   std::vector<rd::LinkConst<double>> L64;
   std::vector<rd::LinkConst<float>> L32;
   std::vector<Rigid> T;            // joint frame of link i expressed in the user's link-i frame
+  bool dh_ok = false;              // DH frames built (all revolute, zero pitch)
+  std::vector<rd::LinkDH<double>> D64;
+  std::vector<rd::LinkDH<float>> D32;
+  Rigid D0;                        // DH base frame in the user's base frame
+  rd::Boundary<double> bdh64;
+  rd::Boundary<float> bdh32;
   double gravity[3] = {0, 0, 0};
   double V0[6] = {0}, Vd0[6] = {0}, Ftip_user[6] = {0};
   rd::Boundary<double> b64;
@@ -177,6 +184,125 @@ void rebuild_boundary(rd_model_t m) {
     m->b32.Vd0[k] = (float)m->Vd0[k];
     m->b32.Ftip[k] = (float)Ft[k];
   }
+  if (m->dh_ok) {
+    // DH base frame D0 is fixed to the base: V''_0 = Ad_{D0^-1} V_0 (same for Vdot_0);
+    // the last DH frame equals link n's joint frame, so F_{n+1} is unchanged.
+    Mat6 Ai;
+    adjoint(rigid_inv(m->D0), Ai);
+    for (int j = 0; j < 6; ++j) {
+      double sv = 0, sa = 0;
+      for (int k = 0; k < 6; ++k) { sv += Ai[j][k] * m->V0[k]; sa += Ai[j][k] * m->Vd0[k]; }
+      m->bdh64.V0[j] = sv; m->bdh64.Vd0[j] = sa; m->bdh64.Ftip[j] = Ft[j];
+      m->bdh32.V0[j] = (float)sv; m->bdh32.Vd0[j] = (float)sa; m->bdh32.Ftip[j] = (float)Ft[j];
+    }
+  }
+}
+
+// Modified-DH (Craig) frames for an all-revolute chain, from the joint frames:
+// G_i = pose of joint frame i in the base at q = 0 (z_i = joint axis).  Frame
+// D_i keeps z_i and puts its origin/x-axis on the common normal of axes i and
+// i+1 (any perpendicular for parallel axes; the joint frame itself for i = n);
+// D_0 := D_1, so f''_{0,1} = Rz(q_1).  Then D_{i-1}^-1 D_i = Rx(alpha) Tx(a)
+// Rz(th0) Tz(d) and the per-link parameters are read off that transform
+// (verified to 1e-10; otherwise the THREAD strategy is not used).
+bool build_dh(rd_model_t m, const std::vector<Rigid>& Mp, const std::vector<std::array<double, 36>>& Jp) {
+  const int n = m->n;
+  std::vector<Rigid> G(n), D(n);
+  Rigid acc = rigid_identity();
+  for (int i = 0; i < n; ++i) { acc = rigid_mul(acc, Mp[i]); G[i] = acc; }
+  auto col = [](const Rigid& g, int c, double* v) { for (int k = 0; k < 3; ++k) v[k] = g.R[k][c]; };
+  auto dot = [](const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; };
+  auto cross = [](const double* a, const double* b, double* c) {
+    c[0] = a[1] * b[2] - a[2] * b[1]; c[1] = a[2] * b[0] - a[0] * b[2]; c[2] = a[0] * b[1] - a[1] * b[0];
+  };
+  for (int i = 0; i < n; ++i) {
+    double z[3], o[3], x[3], P[3];
+    col(G[i], 2, z);
+    for (int k = 0; k < 3; ++k) o[k] = G[i].p[k];
+    if (i == n - 1) {
+      col(G[i], 0, x);
+      for (int k = 0; k < 3; ++k) P[k] = o[k];
+    } else {
+      double z2[3], o2[3], cz[3];
+      col(G[i + 1], 2, z2);
+      for (int k = 0; k < 3; ++k) o2[k] = G[i + 1].p[k];
+      cross(z, z2, cz);
+      const double cn = std::sqrt(dot(cz, cz));
+      double w0[3] = {o[0] - o2[0], o[1] - o2[1], o[2] - o2[2]};
+      if (cn > 1e-9) {
+        const double b = dot(z, z2), dd = dot(z, w0), e = dot(z2, w0), den = 1 - b * b;
+        const double s1 = (b * e - dd) / den, t2 = (e - b * dd) / den;
+        double Q[3];
+        for (int k = 0; k < 3; ++k) { P[k] = o[k] + s1 * z[k]; Q[k] = o2[k] + t2 * z2[k]; }
+        double r[3] = {Q[0] - P[0], Q[1] - P[1], Q[2] - P[2]};
+        const double rn = std::sqrt(dot(r, r));
+        if (rn > 1e-12) for (int k = 0; k < 3; ++k) x[k] = r[k] / rn;
+        else for (int k = 0; k < 3; ++k) x[k] = cz[k] / cn;
+      } else {
+        double r[3] = {o2[0] - o[0], o2[1] - o[1], o2[2] - o[2]};
+        const double rz = dot(r, z);
+        for (int k = 0; k < 3; ++k) r[k] -= rz * z[k];
+        const double rn = std::sqrt(dot(r, r));
+        if (rn > 1e-12) for (int k = 0; k < 3; ++k) x[k] = r[k] / rn;
+        else col(G[i], 0, x);
+        for (int k = 0; k < 3; ++k) P[k] = o[k];
+      }
+    }
+    double y[3];
+    cross(z, x, y);
+    for (int k = 0; k < 3; ++k) {
+      D[i].R[k][0] = x[k]; D[i].R[k][1] = y[k]; D[i].R[k][2] = z[k];
+      D[i].p[k] = P[k];
+    }
+  }
+  m->D0 = D[0];
+  m->D64.resize(n);
+  m->D32.resize(n);
+  for (int i = 0; i < n; ++i) {
+    const Rigid Mi = (i == 0) ? rigid_identity() : rigid_mul(rigid_inv(D[i - 1]), D[i]);
+    const double ca = Mi.R[2][2], sa = -Mi.R[1][2];
+    const double ct = Mi.R[0][0], st = -Mi.R[0][1];
+    const double a = Mi.p[0], d = -sa * Mi.p[1] + ca * Mi.p[2];
+    // verify the DH form R = Rx(alpha) Rz(th0), p = (a, -sa d, ca d)
+    const double Rr[3][3] = {{ct, -st, 0}, {ca * st, ca * ct, -sa}, {sa * st, sa * ct, ca}};
+    double err = std::fabs(Mi.p[1] + sa * d) + std::fabs(Mi.p[2] - ca * d);
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) err += std::fabs(Mi.R[r][c] - Rr[r][c]);
+    if (!(err < 1e-10)) return false;
+    // inertia in the DH frame: E_i = G_i^-1 D_i (a rotation about / slide along z)
+    const Rigid E = rigid_mul(rigid_inv(G[i]), D[i]);
+    Mat6 A;
+    adjoint(E, A);
+    double Jd[6][6];
+    for (int r = 0; r < 6; ++r)
+      for (int c = 0; c < 6; ++c) {
+        double s = 0;
+        for (int k = 0; k < 6; ++k)
+          for (int l = 0; l < 6; ++l) s += A[k][r] * Jp[i][6 * k + l] * A[l][c];
+        Jd[r][c] = s;
+      }
+    rd::LinkDH<double>& L = m->D64[i];
+    L.ca = ca; L.sa = sa;
+    L.p0 = a; L.p1 = -sa * d; L.p2 = ca * d;
+    L.th0 = std::atan2(st, ct);
+    L.cth0 = std::cos(L.th0);
+    L.sth0 = std::sin(L.th0);
+    L.m = (Jd[0][0] + Jd[1][1] + Jd[2][2]) / 3.0;
+    L.h[0] = 0.5 * (Jd[5][1] - Jd[4][2]);
+    L.h[1] = 0.5 * (Jd[3][2] - Jd[5][0]);
+    L.h[2] = 0.5 * (Jd[4][0] - Jd[3][1]);
+    L.I[0] = Jd[3][3]; L.I[1] = Jd[4][4]; L.I[2] = Jd[5][5];
+    L.I[3] = 0.5 * (Jd[3][4] + Jd[4][3]);
+    L.I[4] = 0.5 * (Jd[3][5] + Jd[5][3]);
+    L.I[5] = 0.5 * (Jd[4][5] + Jd[5][4]);
+    rd::LinkDH<float>& F = m->D32[i];
+    F.ca = (float)L.ca; F.sa = (float)L.sa; F.p0 = (float)L.p0; F.p1 = (float)L.p1; F.p2 = (float)L.p2;
+    F.th0 = (float)L.th0; F.m = (float)L.m;
+    F.cth0 = (float)L.cth0; F.sth0 = (float)L.sth0;
+    for (int k = 0; k < 3; ++k) F.h[k] = (float)L.h[k];
+    for (int k = 0; k < 6; ++k) F.I[k] = (float)L.I[k];
+  }
+  return true;
 }
 
 rd_status_t ensure_ws(rd_model_t m, size_t bytes) {
@@ -225,12 +351,15 @@ rd_status_t check_io(rd_model_t m, int64_t batch, const T* a, const T* b, const 
   return RD_OK;
 }
 
-template <typename T> const rd::LinkConst<T>* host_consts(rd_model_t m);
-template <> const rd::LinkConst<double>* host_consts<double>(rd_model_t m) { return m->L64.data(); }
-template <> const rd::LinkConst<float>* host_consts<float>(rd_model_t m) { return m->L32.data(); }
 template <typename T> const rd::LinkConst<T>* dev_consts(rd_model_t m);
 template <> const rd::LinkConst<double>* dev_consts<double>(rd_model_t m) { return m->dL64; }
 template <> const rd::LinkConst<float>* dev_consts<float>(rd_model_t m) { return m->dL32; }
+template <typename T> const rd::LinkDH<T>* dh_consts(rd_model_t m);
+template <> const rd::LinkDH<double>* dh_consts<double>(rd_model_t m) { return m->D64.data(); }
+template <> const rd::LinkDH<float>* dh_consts<float>(rd_model_t m) { return m->D32.data(); }
+template <typename T> const rd::Boundary<T>& dh_bnd(rd_model_t m);
+template <> const rd::Boundary<double>& dh_bnd<double>(rd_model_t m) { return m->bdh64; }
+template <> const rd::Boundary<float>& dh_bnd<float>(rd_model_t m) { return m->bdh32; }
 template <typename T> const rd::Boundary<T>& bnd(rd_model_t m);
 template <> const rd::Boundary<double>& bnd<double>(rd_model_t m) { return m->b64; }
 template <> const rd::Boundary<float>& bnd<float>(rd_model_t m) { return m->b32; }
@@ -246,7 +375,7 @@ constexpr int64_t kWarpScanMaxBatch = 4096;
 
 rd_strategy_t resolve(rd_model_t m, int64_t batch, bool fp64) {
   if (m->strategy == RD_STRAT_GENERIC) return RD_STRAT_GENERIC;
-  const bool thread_ok = m->all_revolute && rd::thread_kernel_has_n(m->n, fp64);
+  const bool thread_ok = m->dh_ok && rd::thread_kernel_has_n(m->n, fp64);
   const bool warp_ok = m->n <= 32;
   if (m->strategy == RD_STRAT_THREAD) return thread_ok ? RD_STRAT_THREAD : RD_STRAT_GENERIC;
   if (m->strategy == RD_STRAT_WARP_SCAN) return warp_ok ? RD_STRAT_WARP_SCAN : RD_STRAT_GENERIC;
@@ -265,7 +394,7 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   cudaError_t e = cudaSuccess;
   if (strat == RD_STRAT_THREAD) {
     bool ok = false;
-    e = rd::launch_rnea_thread<T>(m->n, host_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok);
+    e = rd::launch_rnea_thread<T>(m->n, dh_consts<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok);
     if (!ok) strat = RD_STRAT_GENERIC;
   } else if (strat == RD_STRAT_WARP_SCAN) {
     bool ok = false;
@@ -383,6 +512,8 @@ rd_status_t rd_model_create(int32_t n, const double* M, const double* S, const d
   m->L64.resize(n);
   m->L32.resize(n);
   m->all_revolute = true;
+  std::vector<Rigid> Mps(n);
+  std::vector<std::array<double, 36>> Jps(n);
   // Joint frames: T_i = (R_a, r) with R_a e_z = joint axis and r the point of
   // the axis closest to the link origin; then S'_i = Ad_{T_i^-1} S_i =
   // (beta e_z, alpha e_z), M'_i = T_{i-1}^-1 M_i T_i, J'_i = Ad_{T_i}^T J_i Ad_{T_i}.
@@ -414,6 +545,7 @@ rd_status_t rd_model_create(int32_t n, const double* M, const double* S, const d
     m->T[i] = Ti;
     Rigid Tprev = (i == 0) ? rigid_identity() : m->T[i - 1];
     Rigid Mp = rigid_mul(rigid_mul(rigid_inv(Tprev), rigid_from4(M + 16 * i)), Ti);
+    Mps[i] = Mp;
     Mat6 A;
     adjoint(Ti, A);
     const double* Ji = J + 36 * i;
@@ -424,6 +556,7 @@ rd_status_t rd_model_create(int32_t n, const double* M, const double* S, const d
         for (int k = 0; k < 6; ++k)
           for (int l = 0; l < 6; ++l) s += A[k][a] * Ji[6 * k + l] * A[l][b];
         Jp[a][b] = s;
+        Jps[i][6 * a + b] = s;
       }
     rd::LinkConst<double>& C = m->L64[i];
     for (int a = 0; a < 3; ++a) {
@@ -454,6 +587,7 @@ rd_status_t rd_model_create(int32_t n, const double* M, const double* S, const d
     m->gravity[k] = gravity[k];
     m->Vd0[k] = -gravity[k];     // reading A3: Vdot_0 = (-g, 0)
   }
+  m->dh_ok = m->all_revolute && build_dh(m, Mps, Jps);
   rebuild_boundary(m);
   cudaError_t e = cudaMalloc(&m->dL64, sizeof(rd::LinkConst<double>) * n);
   if (e == cudaSuccess) e = cudaMalloc(&m->dL32, sizeof(rd::LinkConst<float>) * n);

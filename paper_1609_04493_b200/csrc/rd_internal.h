@@ -23,6 +23,22 @@ struct LinkConst {
   T alpha, beta;
 };
 
+// Per-link constants of the all-revolute thread kernel in Denavit-Hartenberg
+// (modified, Craig) frames: f_{i-1,i}(q) =
+// Rx(alpha) Tx(a) Rz(q + th0) Tz(d), i.e. R = Rx(alpha) Rz(q + th0),
+// p = (a, -sin(alpha) d, cos(alpha) d) = (p0, p1, p2); S_i = (0, e_z);
+// inertia as in LinkConst.
+template <typename T>
+struct LinkDH {
+  T ca, sa;       // cos/sin alpha
+  T p0, p1, p2;   // constant translation
+  T th0;          // joint angle offset
+  T cth0, sth0;   // cos/sin th0 (fp32 uses the angle-addition form for accuracy at large |q|)
+  T m;
+  T h[3];
+  T I[6];
+};
+
 // Boundary data of Eq. (3) in the joint frames: V_0, Vdot_0 (base frame,
 // unchanged) and F_{n+1} (expressed in link n's joint frame).
 template <typename T>
@@ -46,7 +62,7 @@ enum Strategy { kAuto = 0, kThread = 1, kWarpScan = 2, kGeneric = 3 };
 // All return cudaGetLastError() after enqueue.  `launches` is incremented by
 // the number of kernels enqueued.
 template <typename T>
-cudaError_t launch_rnea_thread(int n, const LinkConst<T>* L_host, const Boundary<T>& bnd,
+cudaError_t launch_rnea_thread(int n, const LinkDH<T>* L_host, const Boundary<T>& bnd,
                                int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
                                cudaStream_t st, int* launches, bool* supported);
 template <typename T>

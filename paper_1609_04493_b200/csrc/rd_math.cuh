@@ -27,33 +27,54 @@ struct Rot {
 // argument is accurate to ~1 ulp for |x| up to ~1e9); fdlibm minimax
 // polynomials (__kernel_sin / __kernel_cos coefficients) on [-pi/4, pi/4].
 // Measured against the host libm in tests/test_gpu_parity.py (large-angle case).
+// Coefficients in the constant bank so the DFMAs take them as c[][] operands
+// (double literals would be rebuilt with two UMOVs each, every call).
+static __constant__ double kSinCosD[16] = {
+    6755399441055744.0,            // 0: 1.5 * 2^52 (round-to-integer shifter)
+    0.63661977236758138,           // 1: 2/pi
+    1.5707963267948966,            // 2: pi/2 (hi)
+    6.123233995736766e-17,         // 3: pi/2 (lo)
+    1.58969099521155010221e-10,    // 4..9: fdlibm __kernel_sin S6..S1
+    -2.50507602534068634195e-08,
+    2.75573137070700676789e-06,
+    -1.98412698298579493134e-04,
+    8.33333333332248946124e-03,
+    -1.66666666666666324348e-01,
+    -1.13596475577881948265e-11,   // 10..15: fdlibm __kernel_cos C6..C1
+    2.08757232129817482790e-09,
+    -2.75573143513906633035e-07,
+    2.48015872894767294178e-05,
+    -1.38888888888741095749e-03,
+    4.16666666666666019037e-02,
+};
+
 __device__ __forceinline__ void rd_sincos(double x, double* sp, double* cp) {
-  {
-    const double kRound = 6755399441055744.0;              // 1.5 * 2^52
-    const double t = fma(x, 0.63661977236758138, kRound);
-    const int quad = __double2loint(t);
-    const double k = t - kRound;
-    double r = fma(-k, 1.5707963267948966, x);
-    r = fma(-k, 6.123233995736766e-17, r);
-    const double z = r * r;
-    double ps = fma(z, 1.58969099521155010221e-10, -2.50507602534068634195e-08);
-    ps = fma(z, ps, 2.75573137070700676789e-06);
-    ps = fma(z, ps, -1.98412698298579493134e-04);
-    ps = fma(z, ps, 8.33333333332248946124e-03);
-    ps = fma(z, ps, -1.66666666666666324348e-01);
-    const double sn = fma(z * r, ps, r);
-    double pc = fma(z, -1.13596475577881948265e-11, 2.08757232129817482790e-09);
-    pc = fma(z, pc, -2.75573143513906633035e-07);
-    pc = fma(z, pc, 2.48015872894767294178e-05);
-    pc = fma(z, pc, -1.38888888888741095749e-03);
-    pc = fma(z, pc, 4.16666666666666019037e-02);
-    const double cs = fma(z * z, pc, fma(-0.5, z, 1.0));
-    // sin(x) = [s, c, -s, -c][quad & 3], cos(x) = [c, -s, -c, s][quad & 3]
-    const double a = (quad & 1) ? cs : sn;
-    const double b = (quad & 1) ? sn : cs;
-    *sp = (quad & 2) ? -a : a;
-    *cp = ((quad + 1) & 2) ? -b : b;
-  }
+  const double t = fma(x, kSinCosD[1], kSinCosD[0]);
+  const int quad = __double2loint(t);
+  const double k = t - kSinCosD[0];
+  double r = fma(-k, kSinCosD[2], x);
+  r = fma(-k, kSinCosD[3], r);
+  const double z = r * r;
+  double ps = fma(z, kSinCosD[4], kSinCosD[5]);
+  ps = fma(z, ps, kSinCosD[6]);
+  ps = fma(z, ps, kSinCosD[7]);
+  ps = fma(z, ps, kSinCosD[8]);
+  ps = fma(z, ps, kSinCosD[9]);
+  const double sn = fma(z * r, ps, r);
+  double pc = fma(z, kSinCosD[10], kSinCosD[11]);
+  pc = fma(z, pc, kSinCosD[12]);
+  pc = fma(z, pc, kSinCosD[13]);
+  pc = fma(z, pc, kSinCosD[14]);
+  pc = fma(z, pc, kSinCosD[15]);
+  const double cs = fma(z * z, pc, fma(-0.5, z, 1.0));
+  // sin(x) = [s, c, -s, -c][quad & 3], cos(x) = [c, -s, -c, s][quad & 3];
+  // the negations flip the sign bit of the high word.
+  const bool swap = quad & 1;
+  const double a = swap ? cs : sn;
+  const double b = swap ? sn : cs;
+  const unsigned sa = ((unsigned)quad & 2u) << 30, sb = ((unsigned)(quad + 1) & 2u) << 30;
+  *sp = __hiloint2double(__double2hiint(a) ^ (int)sa, __double2loint(a));
+  *cp = __hiloint2double(__double2hiint(b) ^ (int)sb, __double2loint(b));
 }
 // fp32: three-float Cody-Waite split of pi/2 (accurate for |x| up to ~1e4) and
 // Cephes minimax polynomials; branch-free.
@@ -119,8 +140,9 @@ __device__ __forceinline__ void ad_finv(const Rot<T>& R, T p0, T p1, T p2, const
 }
 
 // Fhat = J Vd + (w x P_f, v x P_f + w x P_m), P = J V
-template <typename T>
-__device__ __forceinline__ void bias_force(const LinkConst<T>& C, const T* V, const T* Vd, T* Fh) {
+// CT: any per-link constant struct with m, h[3], I[6] (LinkConst or LinkDH).
+template <typename T, typename CT>
+__device__ __forceinline__ void bias_force(const CT& C, const T* V, const T* Vd, T* Fh) {
   const T m = C.m, h0 = C.h[0], h1 = C.h[1], h2 = C.h[2];
   const T Ixx = C.I[0], Iyy = C.I[1], Izz = C.I[2], Ixy = C.I[3], Ixz = C.I[4], Iyz = C.I[5];
   // P = J V
@@ -184,6 +206,42 @@ __device__ __forceinline__ void bwd_step(const Rot<T>& R, T p0, T p1, T p2, cons
   T y0, y1, y2, z0, z1, z2;
   rot_n(R, Fn[0], Fn[1], Fn[2], y0, y1, y2);
   rot_n(R, Fn[3], Fn[4], Fn[5], z0, z1, z2);
+  F[0] = Fh[0] + y0;
+  F[1] = Fh[1] + y1;
+  F[2] = Fh[2] + y2;
+  F[3] = fma(p1, y2, fma(-p2, y1, Fh[3] + z0));
+  F[4] = fma(p2, y0, fma(-p0, y2, Fh[4] + z1));
+  F[5] = fma(p0, y1, fma(-p1, y0, Fh[5] + z2));
+}
+
+// ---------------------------------------------------------------- DH frames
+// f = (R, p), R = Rx(alpha) Rz(theta), p = (p0, p1, p2) constant (LinkDH).
+// out = Ad_{f^-1} in = (R^T (v + w x p), R^T w), R^T = Rz^T Rx^T.
+template <typename T>
+__device__ __forceinline__ void dh_ad_finv(const LinkDH<T>& C, T s, T c, const T* in, T* out) {
+  const T x0 = fma(in[4], C.p2, fma(-in[5], C.p1, in[0]));
+  const T x1 = fma(in[5], C.p0, fma(-in[3], C.p2, in[1]));
+  const T x2 = fma(in[3], C.p1, fma(-in[4], C.p0, in[2]));
+  // Rx^T x = (x0, ca x1 + sa x2, -sa x1 + ca x2); then Rz^T y = (c y0 + s y1, -s y0 + c y1, y2)
+  const T y1 = fma(C.ca, x1, C.sa * x2), y2 = fma(C.ca, x2, -(C.sa * x1));
+  out[0] = fma(c, x0, s * y1);
+  out[1] = fma(c, y1, -(s * x0));
+  out[2] = y2;
+  const T u1 = fma(C.ca, in[4], C.sa * in[5]), u2 = fma(C.ca, in[5], -(C.sa * in[4]));
+  out[3] = fma(c, in[3], s * u1);
+  out[4] = fma(c, u1, -(s * in[3]));
+  out[5] = u2;
+}
+
+// F = Fh + Ad^T_{f^-1} Fn = Fh + (R f, p x (R f) + R m), R = Rx(alpha) Rz(theta)
+// with (ca, sa, p, s, c) of the child link (identity for the tip, A5).
+template <typename T>
+__device__ __forceinline__ void dh_bwd(T ca, T sa, T p0, T p1, T p2, T s, T c, const T* Fn, const T* Fh, T* F) {
+  // Rz y = (c y0 - s y1, s y0 + c y1, y2); Rx z = (z0, ca z1 - sa z2, sa z1 + ca z2)
+  const T a0 = fma(c, Fn[0], -(s * Fn[1])), a1 = fma(s, Fn[0], c * Fn[1]), a2 = Fn[2];
+  const T y0 = a0, y1 = fma(ca, a1, -(sa * a2)), y2 = fma(sa, a1, ca * a2);
+  const T b0 = fma(c, Fn[3], -(s * Fn[4])), b1 = fma(s, Fn[3], c * Fn[4]), b2 = Fn[5];
+  const T z0 = b0, z1 = fma(ca, b1, -(sa * b2)), z2 = fma(sa, b1, ca * b2);
   F[0] = Fh[0] + y0;
   F[1] = Fh[1] + y1;
   F[2] = Fh[2] + y2;

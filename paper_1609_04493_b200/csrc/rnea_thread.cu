@@ -28,10 +28,11 @@ constexpr int kMaxThreadN = 32;
 
 template <typename T>
 struct ThreadParams {
-  LinkConst<T> L[kMaxThreadN];
+  LinkDH<T> L[kMaxThreadN];
   Boundary<T> bnd;
   int n;          // links
   int lt;         // links stashed in TMEM (the rest in shared memory)
+  int l2ahead;    // L2 prefetch distance in links (0 = off; RD_L2AHEAD experiment knob)
 };
 
 // ------------------------------------------------------------------ TMEM helpers
@@ -108,132 +109,6 @@ template <> struct TmemIO<float> {
   }
 };
 
-// ------------------------------------------------------------------ kernel
-// W warps per CTA; one CTA per SM (it owns all 512 TMEM columns).
-template <typename T, int W>
-__global__ void __launch_bounds__(W * 32, 1)
-rnea_thread_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
-                   const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
-                   T* __restrict__ tau) {
-  constexpr int NT = W * 32;
-  constexpr int kColsPerWarp = 2048 / W;          // 512 columns x 4 lane quarters / W warps
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sstash = reinterpret_cast<T*>(smem_raw);     // [n - lt][8][NT]
-  __shared__ uint32_t tmem_slot;
-
-  const int warp = threadIdx.x >> 5;
-  const int tid = threadIdx.x;
-  if (warp == 0) tmem_alloc_512(&tmem_slot);
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tbase = tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * kColsPerWarp);
-
-  const int n = P.n, lt = P.lt;
-  const int64_t ntiles = (B + NT - 1) / NT;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t b = tile * NT + tid;
-    const bool valid = b < B;
-    const int64_t bl = valid ? b : (B - 1);       // clamped: every lane joins the .sync.aligned TMEM ops
-    const T* pq = q + bl;
-    const T* pqd = qd + bl;
-    const T* pqa = qdd + bl;
-
-    // ---------------- forward sweep, Eq. (1): f_i, V_i, Vdot_i, then Fhat_i
-    T V[6], Vd[6];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) { V[k] = P.bnd.V0[k]; Vd[k] = P.bnd.Vd0[k]; }
-    T c_q = __ldg(pq), c_qd = __ldg(pqd), c_qa = __ldg(pqa);
-    const int64_t off1 = (n > 1 ? 1 : 0) * B;
-    T n_q = __ldg(pq + off1), n_qd = __ldg(pqd + off1), n_qa = __ldg(pqa + off1);
-#pragma unroll 2
-    for (int i = 0; i < n; ++i) {
-      const int64_t off2 = (int64_t)min(i + 2, n - 1) * B;
-      const T f_q = __ldg(pq + off2), f_qd = __ldg(pqd + off2), f_qa = __ldg(pqa + off2);
-      const LinkConst<T>& C = P.L[i];
-      T s, c;
-      rd_sincos(c_q, &s, &c);
-      const Rot<T> R = make_rot(C, s, c);
-      T Vn[6], Vdn[6];
-      fwd_step<T, true>(C, R, C.pm[0], C.pm[1], C.pm[2], c_qd, c_qa, V, Vd, Vn, Vdn);
-      T st[8];
-      st[0] = s;
-      st[1] = c;
-      bias_force(C, Vn, Vdn, st + 2);
-      if (i < lt) {
-        TmemIO<T>::st(tbase + (uint32_t)(i * TmemIO<T>::kCols), st);
-      } else {
-        T* d = sstash + (size_t)(i - lt) * 8 * NT + tid;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) d[k * NT] = st[k];
-      }
-#pragma unroll
-      for (int k = 0; k < 6; ++k) { V[k] = Vn[k]; Vd[k] = Vdn[k]; }
-      c_q = n_q; c_qd = n_qd; c_qa = n_qa;
-      n_q = f_q; n_qd = f_qd; n_qa = f_qa;
-    }
-    tmem_wait_st();
-
-    // ---------------- backward sweep, Eq. (2):
-    // F_n = Fhat_n + F_{n+1}, F_i = Fhat_i + Ad^T_{f_{i,i+1}^{-1}} F_{i+1}, tau_i = F_i[5] (joint frame).
-    T F[6];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) F[k] = P.bnd.Ftip[k];
-    Rot<T> Rn;
-    T pn0 = 0, pn1 = 0, pn2 = 0;
-    bool tip = true;
-    T* tcol = tau + b;
-    // (a) links in shared memory, i = n-1 .. lt
-    for (int i = n - 1; i >= lt; --i) {
-      const T* d = sstash + (size_t)(i - lt) * 8 * NT + tid;
-      T cur[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) cur[k] = d[k * NT];
-      if (tip) {
-#pragma unroll
-        for (int k = 0; k < 6; ++k) F[k] += cur[2 + k];
-        tip = false;
-      } else {
-        T Fo[6];
-        bwd_step(Rn, pn0, pn1, pn2, F, cur + 2, Fo);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) F[k] = Fo[k];
-      }
-      if (valid) tcol[(int64_t)i * B] = F[5];
-      const LinkConst<T>& C = P.L[i];
-      Rn = make_rot(C, cur[0], cur[1]);
-      pn0 = C.pm[0]; pn1 = C.pm[1]; pn2 = C.pm[2];
-    }
-    // (b) links in TMEM, i = lt-1 .. 0, with the next link's tcgen05.ld in flight
-    typename TmemIO<T>::Regs rA;
-    if (lt > 0) TmemIO<T>::ld(tbase + (uint32_t)((lt - 1) * TmemIO<T>::kCols), rA);
-    for (int i = lt - 1; i >= 0; --i) {
-      TmemIO<T>::wait(rA);
-      T cur[8];
-      TmemIO<T>::unpack(rA, cur);
-      if (i > 0) TmemIO<T>::ld(tbase + (uint32_t)((i - 1) * TmemIO<T>::kCols), rA);
-      if (tip) {
-#pragma unroll
-        for (int k = 0; k < 6; ++k) F[k] += cur[2 + k];
-        tip = false;
-      } else {
-        T Fo[6];
-        bwd_step(Rn, pn0, pn1, pn2, F, cur + 2, Fo);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) F[k] = Fo[k];
-      }
-      if (valid) tcol[(int64_t)i * B] = F[5];
-      const LinkConst<T>& C = P.L[i];
-      Rn = make_rot(C, cur[0], cur[1]);
-      pn0 = C.pm[0]; pn1 = C.pm[1]; pn2 = C.pm[2];
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  if (warp == 0) tmem_dealloc_512(tmem_slot);
-}
-
 // ------------------------------------------------------------------ ping-pong kernel
 // Same arithmetic, but the backward sweep of tile t-1 and the forward sweep of
 // tile t run in the SAME loop (step k: backward of link n-1-k, forward of link
@@ -253,8 +128,7 @@ struct FwdState {
 template <typename T>
 struct BwdState {
   T F[6];
-  Rot<T> Rn;
-  T pn0, pn1, pn2;
+  T ca, sa, p0, p1, p2, s, c;   // DH constants and stashed (sin, cos) of the child link i+1
   int64_t b;
   bool valid;
 };
@@ -273,8 +147,7 @@ template <typename T>
 __device__ __forceinline__ void bwd_init(BwdState<T>& g, const ThreadParams<T>& P) {
 #pragma unroll
   for (int k = 0; k < 6; ++k) g.F[k] = P.bnd.Ftip[k];
-  g.Rn = Rot<T>{1, 0, 0, 0, 1, 0, 0, 0, 1};     // f_{n,n+1} = I (A5)
-  g.pn0 = g.pn1 = g.pn2 = 0;
+  g.ca = 1; g.sa = 0; g.p0 = g.p1 = g.p2 = 0; g.s = 0; g.c = 1;   // f_{n,n+1} = I (A5)
 }
 // forward link k: V_k, Vdot_k, Fhat_k -> st[8]
 template <typename T>
@@ -282,12 +155,32 @@ __device__ __forceinline__ void fwd_link(FwdState<T>& f, const ThreadParams<T>& 
   const int n = P.n;
   const int64_t off2 = (int64_t)min(k + 2, n - 1) * B;
   const T f_q = __ldg(f.pq + off2), f_qd = __ldg(f.pqd + off2), f_qa = __ldg(f.pqa + off2);
-  const LinkConst<T>& C = P.L[k];
+  if (P.l2ahead > 0) {                            // experiment knob: pull link k+l2ahead into L2
+    const int64_t offp = (int64_t)min(k + P.l2ahead, n - 1) * B;
+    asm volatile("prefetch.global.L2 [%0];" :: "l"(f.pq + offp));
+    asm volatile("prefetch.global.L2 [%0];" :: "l"(f.pqd + offp));
+    asm volatile("prefetch.global.L2 [%0];" :: "l"(f.pqa + offp));
+  }
+  const LinkDH<T>& C = P.L[k];
   T s, c;
-  rd_sincos(f.c_q, &s, &c);
-  const Rot<T> R = make_rot(C, s, c);
+  if (sizeof(T) == 8) {
+    rd_sincos(f.c_q + C.th0, &s, &c);            // fp64: rounding of q + th0 is ~ulp(q)
+  } else {
+    T s0, c0;                                     // fp32: sin/cos(q) then add th0 exactly
+    rd_sincos(f.c_q, &s0, &c0);
+    s = fma(s0, C.cth0, c0 * C.sth0);
+    c = fma(c0, C.cth0, -(s0 * C.sth0));
+  }
+  // Eq. (1): V = Ad_{f^-1} V + S qd, Vd = Ad_{f^-1} Vd + S qdd + ad_V(S qd), S = (0, e_z)
   T Vn[6], Vdn[6];
-  fwd_step<T, true>(C, R, C.pm[0], C.pm[1], C.pm[2], f.c_qd, f.c_qa, f.V, f.Vd, Vn, Vdn);
+  dh_ad_finv(C, s, c, f.V, Vn);
+  dh_ad_finv(C, s, c, f.Vd, Vdn);
+  Vn[5] += f.c_qd;
+  Vdn[5] += f.c_qa;
+  Vdn[0] = fma(f.c_qd, Vn[1], Vdn[0]);
+  Vdn[1] = fma(-f.c_qd, Vn[0], Vdn[1]);
+  Vdn[3] = fma(f.c_qd, Vn[4], Vdn[3]);
+  Vdn[4] = fma(-f.c_qd, Vn[3], Vdn[4]);
   st[0] = s;
   st[1] = c;
   bias_force(C, Vn, Vdn, st + 2);
@@ -301,13 +194,13 @@ template <typename T>
 __device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& P, int64_t B, int i,
                                          const T* cur, T* __restrict__ tau) {
   T Fo[6];
-  bwd_step(g.Rn, g.pn0, g.pn1, g.pn2, g.F, cur + 2, Fo);
+  dh_bwd(g.ca, g.sa, g.p0, g.p1, g.p2, g.s, g.c, g.F, cur + 2, Fo);
 #pragma unroll
   for (int j = 0; j < 6; ++j) g.F[j] = Fo[j];
   if (g.valid) tau[(int64_t)i * B + g.b] = g.F[5];
-  const LinkConst<T>& C = P.L[i];
-  g.Rn = make_rot(C, cur[0], cur[1]);
-  g.pn0 = C.pm[0]; g.pn1 = C.pm[1]; g.pn2 = C.pm[2];
+  const LinkDH<T>& C = P.L[i];
+  g.ca = C.ca; g.sa = C.sa; g.p0 = C.p0; g.p1 = C.p1; g.p2 = C.p2;
+  g.s = cur[0]; g.c = cur[1];
 }
 
 template <typename T, int W>
@@ -472,26 +365,20 @@ bool thread_kernel_has_n(int n, bool fp64) {
   return fp64 ? plan_for<double>(n, &p) : plan_for<float>(n, &p);
 }
 
-template <typename T, int W, bool PP>
+template <typename T, int W>
 static cudaError_t launch_w(const ThreadParams<T>& P, size_t smem, int64_t B, const T* q, const T* qd,
                             const T* qdd, T* tau, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(PP ? (const void*)rnea_thread_pp_kernel<T, W> : (const void*)rnea_thread_kernel<T, W>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(kSmemCap - 1024));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = cudaFuncSetAttribute(rnea_thread_pp_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(kSmemCap - 1024));
+  if (e != cudaSuccess) return e;
   const int64_t ntiles = (B + W * 32 - 1) / (W * 32);
   const int64_t grid = ntiles < num_sms() ? ntiles : num_sms();
-  if (PP) rnea_thread_pp_kernel<T, W><<<(unsigned)grid, W * 32, smem, st>>>(P, B, q, qd, qdd, tau);
-  else rnea_thread_kernel<T, W><<<(unsigned)grid, W * 32, smem, st>>>(P, B, q, qd, qdd, tau);
+  rnea_thread_pp_kernel<T, W><<<(unsigned)grid, W * 32, smem, st>>>(P, B, q, qd, qdd, tau);
   return cudaGetLastError();
 }
 
 template <typename T>
-cudaError_t launch_rnea_thread(int n, const LinkConst<T>* L_host, const Boundary<T>& bnd, int64_t B,
+cudaError_t launch_rnea_thread(int n, const LinkDH<T>* L_host, const Boundary<T>& bnd, int64_t B,
                                const T* q, const T* qd, const T* qdd, T* tau, cudaStream_t st,
                                int* launches, bool* supported) {
   StashPlan plan;
@@ -502,18 +389,17 @@ cudaError_t launch_rnea_thread(int n, const LinkConst<T>* L_host, const Boundary
   P.bnd = bnd;
   P.n = n;
   P.lt = plan.lt;
+  static const int l2a = getenv("RD_L2AHEAD") ? atoi(getenv("RD_L2AHEAD")) : 0;
+  P.l2ahead = l2a;
   ++*launches;
-  static const bool pipe = !(getenv("RD_PP") && getenv("RD_PP")[0] == '0');   // ping-pong default
-  if (plan.W == 16) return pipe ? launch_w<T, 16, true>(P, plan.smem, B, q, qd, qdd, tau, st)
-                                : launch_w<T, 16, false>(P, plan.smem, B, q, qd, qdd, tau, st);
-  return pipe ? launch_w<T, 8, true>(P, plan.smem, B, q, qd, qdd, tau, st)
-              : launch_w<T, 8, false>(P, plan.smem, B, q, qd, qdd, tau, st);
+  if (plan.W == 16) return launch_w<T, 16>(P, plan.smem, B, q, qd, qdd, tau, st);
+  return launch_w<T, 8>(P, plan.smem, B, q, qd, qdd, tau, st);
 }
 
-template cudaError_t launch_rnea_thread<double>(int, const LinkConst<double>*, const Boundary<double>&, int64_t,
+template cudaError_t launch_rnea_thread<double>(int, const LinkDH<double>*, const Boundary<double>&, int64_t,
                                                 const double*, const double*, const double*, double*,
                                                 cudaStream_t, int*, bool*);
-template cudaError_t launch_rnea_thread<float>(int, const LinkConst<float>*, const Boundary<float>&, int64_t,
+template cudaError_t launch_rnea_thread<float>(int, const LinkDH<float>*, const Boundary<float>&, int64_t,
                                                const float*, const float*, const float*, float*,
                                                cudaStream_t, int*, bool*);
 

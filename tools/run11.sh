@@ -1,0 +1,2 @@
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x 2>&1 | grep -E "FAILED|Error|assert|passed|failed" | head -20
+timeout 300 python tools/quick_time.py 2>&1 | grep -E "C3 float|C4"
