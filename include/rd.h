@@ -18,8 +18,8 @@
  *
  * Memory: batch arrays are structure-of-arrays, link-major: x[i*batch + b] for
  * link i (0-based) and state b; `lda` variants are not provided.  Device
- * pointers must be 16-byte aligned device memory of the current CUDA device;
- * outputs must not alias inputs.  The caller owns every I/O buffer; the model
+ * pointers must be naturally aligned (8 B fp64, 4 B fp32) device memory of the
+ * current CUDA device (checked: RD_E_ARG otherwise); outputs must not alias inputs.  The caller owns every I/O buffer; the model
  * owns its constants and any workspace.
  *
  * Errors: every call returns rd_status_t; RD_OK == 0.  rd_last_error() returns
@@ -61,7 +61,8 @@ typedef enum {
 /* Forward-dynamics algorithm. */
 typedef enum {
   RD_FD_ABA = 0,          /* articulated-body algorithm, Eq. (7)-(8), Alg. 3 (default) */
-  RD_FD_JSIIA = 1         /* joint-space inertia inversion, Eq. (6)/(17), Alg. 2 (Cholesky) */
+  RD_FD_JSIIA = 1         /* joint-space inertia inversion, Eq. (6)/(17), Alg. 2: n+1 IDs per state
+                             (one per lane of a warp) + Cholesky solve; n <= 31, else RD_E_UNSUPPORTED */
 } rd_fd_algo_t;
 
 /* Library version string. */

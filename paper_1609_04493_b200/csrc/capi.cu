@@ -420,6 +420,14 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   rd_status_t st = check_io<T>(m, batch, q, qd, tau, qdd, true);
   if (st != RD_OK || batch == 0) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (m->fd_algo == RD_FD_JSIIA) {
+    bool ok = false;
+    cudaError_t e = rd::launch_jsiia<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd, s,
+                                        &g_launches, &ok);
+    if (!ok) return fail(RD_E_UNSUPPORTED, "JSIIA forward dynamics supports n <= 31 (use RD_FD_ABA)");
+    if (e != cudaSuccess) return cuda_fail(e, "forward dynamics (JSIIA) launch");
+    return RD_OK;
+  }
   std::lock_guard<std::mutex> lk(m->mu);
   const int64_t slots = rd::generic_ws_slots(batch);
   st = ensure_ws(m, (size_t)slots * m->n * rd::aba_ws_per_link() * sizeof(T));

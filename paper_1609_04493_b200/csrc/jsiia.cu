@@ -1,0 +1,195 @@
+// jsiia.cu -- forward dynamics by joint-space inertia inversion, Alg. 2
+// (Eq. 5, 6, 17): one WARP per state, the n+1 data-independent
+// inverse dynamics of Alg. 2 line 1 run one per LANE ("All n+1 inverse
+// dynamics are data independent, and thus may be solved simultaneously"):
+//   lane j < n : M_{.,j} = ID(q, 0, delta_{.,j}, 0, 0, 0)          (Eq. 17)
+//   lane n     : tau_bias = ID(q, qd, 0, V_0, Vdot_0, F_{n+1})      (Eq. 5)
+// then tau_diff = tau - tau_bias (line 2) and a warp-cooperative Cholesky
+// factorisation and two triangular solves in shared memory instead of the
+// explicit inverse of lines 3-4 (the paper points to parallel Cholesky).
+//
+// Each lane's RNEA keeps no per-link stash: the backward sweep re-derives V_i,
+// Vdot_i by inverting the (rigid, well-conditioned) forward maps,
+// V_{i-1} = Ad_{f_i}(V_i - S_i qd_i),
+// Vdot_{i-1} = Ad_{f_i}(Vdot_i - S_i qdd_i - ad_{V_i}(S_i qd_i)),
+// so the whole ID runs in registers; the link transforms (sin, cos, d) are
+// computed once per state by lane i and shared through shared memory.
+// n <= 31.  A non-SPD M (pivot <= 0) makes that state's qdd NaN (A11).
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "rd_internal.h"
+#include "rd_math.cuh"
+
+namespace rd {
+
+constexpr int kJsWarps = 4;
+
+// out = Ad_f in = (R v + p x (R w), R w)
+template <typename T>
+__device__ __forceinline__ void ad_f(const Rot<T>& R, T p0, T p1, T p2, const T* in, T* out) {
+  T w0, w1, w2;
+  rot_n(R, in[3], in[4], in[5], w0, w1, w2);
+  T v0, v1, v2;
+  rot_n(R, in[0], in[1], in[2], v0, v1, v2);
+  out[0] = fma(p1, w2, fma(-p2, w1, v0));
+  out[1] = fma(p2, w0, fma(-p0, w2, v1));
+  out[2] = fma(p0, w1, fma(-p1, w0, v2));
+  out[3] = w0; out[4] = w1; out[5] = w2;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kJsWarps * 32)
+jsiia_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
+             const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ tau_in,
+             T* __restrict__ qdd_out) {
+  constexpr int NF = sizeof(LinkConst<T>) / sizeof(T);
+  __shared__ T sc[NF][32];                  // link constants [field][link]
+  __shared__ T strf[kJsWarps][3][32];       // per-state link transforms (sin, cos, d)
+  __shared__ T sM[kJsWarps][32][33];        // M(q), then its Cholesky factor (lower)
+  for (int idx = threadIdx.x; idx < NF * 32; idx += blockDim.x) {
+    const int f = idx / 32, l = idx % 32;
+    sc[f][l] = l < n ? reinterpret_cast<const T*>(Lg + l)[f] : T(0);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned full = 0xffffffffu;
+  auto cst = [&](int i) {
+    LinkConst<T> C;
+#pragma unroll
+    for (int f = 0; f < 9; ++f) C.Rm[f] = sc[f][i];
+#pragma unroll
+    for (int f = 0; f < 3; ++f) { C.pm[f] = sc[9 + f][i]; C.h[f] = sc[13 + f][i]; }
+    C.m = sc[12][i];
+#pragma unroll
+    for (int f = 0; f < 6; ++f) C.I[f] = sc[16 + f][i];
+    C.alpha = sc[22][i];
+    C.beta = sc[23][i];
+    return C;
+  };
+  T (*M)[33] = sM[warp];
+  for (int64_t b = (int64_t)blockIdx.x * kJsWarps + warp; b < B; b += (int64_t)gridDim.x * kJsWarps) {
+    // CalcTransform: lane l owns link l
+    T qdl = 0, taul = 0;
+    if (lane < n) {
+      const T ql = __ldg(q + (int64_t)lane * B + b);
+      qdl = __ldg(qd + (int64_t)lane * B + b);
+      taul = __ldg(tau_in + (int64_t)lane * B + b);
+      T s, c;
+      rd_sincos(sc[22][lane] * ql, &s, &c);
+      strf[warp][0][lane] = s;
+      strf[warp][1][lane] = c;
+      strf[warp][2][lane] = sc[23][lane] * ql;
+    }
+    __syncwarp();
+    const bool bias = lane == n;
+    // ---- forward sweep of this lane's ID
+    T V[6], Vd[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) { V[k] = bias ? bnd.V0[k] : T(0); Vd[k] = bias ? bnd.Vd0[k] : T(0); }
+    for (int i = 0; i < n; ++i) {
+      const LinkConst<T> C = cst(i);
+      const T s = strf[warp][0][i], c = strf[warp][1][i], d = strf[warp][2][i];
+      const Rot<T> R = make_rot(C, s, c);
+      const T p0 = fma(d, C.Rm[2], C.pm[0]), p1 = fma(d, C.Rm[5], C.pm[1]), p2 = fma(d, C.Rm[8], C.pm[2]);
+      const T qds = __shfl_sync(full, qdl, i);        // every lane joins the shuffle
+      const T qdi = bias ? qds : T(0);
+      const T qddi = (lane == i) ? T(1) : T(0);
+      T Vn[6], Vdn[6];
+      fwd_step<T, false>(C, R, p0, p1, p2, qdi, qddi, V, Vd, Vn, Vdn);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) { V[k] = Vn[k]; Vd[k] = Vdn[k]; }
+    }
+    // ---- backward sweep: F_i = Fhat_i + Ad^T F_{i+1}; tau_i = S_i^T F_i; then invert the forward map
+    T F[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) F[k] = bias ? bnd.Ftip[k] : T(0);
+    Rot<T> Rn{1, 0, 0, 0, 1, 0, 0, 0, 1};
+    T pn0 = 0, pn1 = 0, pn2 = 0;
+    for (int i = n - 1; i >= 0; --i) {
+      const LinkConst<T> C = cst(i);
+      T Fh[6], Fo[6];
+      bias_force(C, V, Vd, Fh);
+      bwd_step(Rn, pn0, pn1, pn2, F, Fh, Fo);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) F[k] = Fo[k];
+      const T ti = fma(C.beta, F[2], C.alpha * F[5]);
+      if (lane < n) M[i][lane] = ti;            // column j = lane of M(q), Eq. (17)
+      if (bias) M[i][31] = ti;                  // tau_bias (n <= 31 keeps column 31 free)
+      // rebuild V_{i-1}, Vdot_{i-1}
+      const T s = strf[warp][0][i], c = strf[warp][1][i], d = strf[warp][2][i];
+      Rn = make_rot(C, s, c);
+      pn0 = fma(d, C.Rm[2], C.pm[0]); pn1 = fma(d, C.Rm[5], C.pm[1]); pn2 = fma(d, C.Rm[8], C.pm[2]);
+      const T qds = __shfl_sync(full, qdl, i);        // every lane joins the shuffle
+      const T qdi = bias ? qds : T(0);
+      const T qddi = (lane == i) ? T(1) : T(0);
+      const T a = C.alpha, be = C.beta, aq = a * qdi, bq = be * qdi;
+      T x[6], y[6];
+      // Vdot_i - S qdd - ad_{V_i}(S qd); ad_V(S qd) = qd (beta w x e_z + alpha v x e_z, alpha w x e_z)
+      y[0] = Vd[0] - fma(bq, V[4], aq * V[1]);
+      y[1] = Vd[1] + fma(bq, V[3], aq * V[0]);
+      y[2] = Vd[2] - be * qddi;
+      y[3] = Vd[3] - aq * V[4];
+      y[4] = Vd[4] + aq * V[3];
+      y[5] = Vd[5] - a * qddi;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) x[k] = V[k];
+      x[2] -= bq;
+      x[5] -= aq;
+      ad_f(Rn, pn0, pn1, pn2, x, V);
+      ad_f(Rn, pn0, pn1, pn2, y, Vd);
+    }
+    __syncwarp();
+    // ---- tau_diff = tau - tau_bias; Cholesky M = L L^T; solve (Alg. 2 lines 2-4)
+    T rhs = (lane < n) ? taul - M[lane][31] : T(0);
+    bool spd = true;
+    for (int k = 0; k < n; ++k) {
+      const T piv = M[k][k];
+      spd = spd && (piv > T(0));
+      const T lkk = sqrt(piv > T(0) ? piv : T(1));
+      __syncwarp();
+      if (lane > k && lane < n) M[lane][k] /= lkk;
+      __syncwarp();
+      if (lane > k && lane < n) {
+        const T lik = M[lane][k];
+        for (int j = k + 1; j <= lane; ++j) M[lane][j] = fma(-lik, M[j][k], M[lane][j]);
+      }
+      if (lane == k) M[k][k] = lkk;
+      __syncwarp();
+    }
+    // L y = rhs (column sweep), then L^T x = y
+    for (int i = 0; i < n; ++i) {
+      const T yi = __shfl_sync(full, rhs, i) / M[i][i];
+      if (lane == i) rhs = yi;
+      if (lane > i && lane < n) rhs = fma(-M[lane][i], yi, rhs);
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      const T xi = __shfl_sync(full, rhs, i) / M[i][i];
+      if (lane == i) rhs = xi;
+      if (lane < i) rhs = fma(-M[i][lane], xi, rhs);
+    }
+    if (lane < n) qdd_out[(int64_t)lane * B + b] = spd ? rhs : T(NAN);
+    __syncwarp();
+  }
+}
+
+template <typename T>
+cudaError_t launch_jsiia(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
+                         const T* qd, const T* tau, T* qdd, cudaStream_t st, int* launches, bool* supported) {
+  *supported = n >= 1 && n <= 31;
+  if (!*supported) return cudaSuccess;
+  int64_t grid = (B + kJsWarps - 1) / kJsWarps;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (grid > cap) grid = cap;
+  jsiia_kernel<T><<<(unsigned)grid, kJsWarps * 32, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_jsiia<double>(int, const LinkConst<double>*, const Boundary<double>&, int64_t,
+                                          const double*, const double*, const double*, double*, cudaStream_t,
+                                          int*, bool*);
+template cudaError_t launch_jsiia<float>(int, const LinkConst<float>*, const Boundary<float>&, int64_t,
+                                         const float*, const float*, const float*, float*, cudaStream_t, int*,
+                                         bool*);
+
+}  // namespace rd

@@ -78,6 +78,11 @@ cudaError_t launch_aba(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                        int64_t B, const T* q, const T* qd, const T* tau, T* qdd,
                        T* ws, int64_t ws_slots, cudaStream_t st, int* launches);
 
+template <typename T>
+cudaError_t launch_jsiia(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
+                         int64_t B, const T* q, const T* qd, const T* tau, T* qdd,
+                         cudaStream_t st, int* launches, bool* supported);
+
 // Workspace slots (threads) the generic / ABA kernels use: ws holds
 // per-link doubles for each slot (see the .cu files for the layout).
 int64_t generic_ws_slots(int64_t B);

@@ -284,3 +284,38 @@ def test_thread_kernel_many_tiles(rd):
     q, qd, qdd = synth.states(cfg["seed"], 30, 0, 70000)
     check_id(rd, synth.robot_for(cfg), cfg["gravity"], q, qd, qdd, strategy="thread",
              sample=np.arange(0, 70000, 7))
+
+
+# ------------------------------------------------------------------ forward dynamics (JSIIA, NEXT-1)
+@pytest.mark.parametrize("n,pf", [(1, 0.0), (2, 0.0), (7, 0.3), (10, 0.0), (30, 0.0), (31, 0.2)])
+def test_fd_jsiia_parity(rd, n, pf):
+    r = synth.random_chain(n, 700 + n, prismatic_fraction=pf)
+    g = synth.GRAVITY_Z
+    q, qd, qdd = synth.states(17, n, 0, 1500)
+    tau = oracle.rnea_batch(r, g, q, qd, qdd)
+    model = rd.Model.from_robot(r, g)
+    model.set_fd_algo("jsiia")
+    out = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()
+    assert np.all(np.isfinite(out))
+    back = oracle.rnea_batch(r, g, q, qd, out)
+    assert rel_err_per_state(back, tau).max() <= 1e-10
+    ref = oracle.fd_batch(r, g, q, qd, tau, algo="jsiia")
+    assert rel_err_per_state(out, ref, floor=1.0).max() < 1e-7
+
+
+def test_fd_jsiia_boundary_and_limits(rd):
+    r = synth.random_chain(6, 44)
+    rng = np.random.default_rng(3)
+    V0, Vd0, Ft = rng.standard_normal((3, 6))
+    model = rd.Model.from_robot(r, (0, 0, 0))
+    model.set_boundary(V0, Vd0, Ft)
+    model.set_fd_algo("jsiia")
+    q, qd, qdd = synth.states(9, 6, 0, 300)
+    tau = np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b], V0, Vd0, Ft) for b in range(300)], 1)
+    out = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()
+    assert rel_err_per_state(out, qdd, floor=1.0).max() < 1e-9
+    big = rd.Model.from_robot(synth.random_chain(40, 1), synth.GRAVITY_Z)
+    big.set_fd_algo("jsiia")
+    z = torch.zeros((40, 10), dtype=torch.float64, device="cuda")
+    with pytest.raises(rd.RdError):
+        rd.forward_dynamics(big, z, z, z)
