@@ -14,7 +14,10 @@
 //      (the articulated-bias recursion plays the role of Eq. (18)/(20))
 //   3. forward (the role of Eq. 19): a'_i = X_i a_{i-1} + c_i (a_0 = Vdot_0),
 //      qdd_i = (u_i - U_i^T a'_i) / D_i,  a_i = a'_i + S_i qdd_i.
-// X_i = Ad_{f_{i-1,i}^{-1}}.  Per-state scratch (17 scalars per link) lives in a
+// X_i = Ad_{f_{i-1,i}^{-1}}.  Memory-lean: sweeps 1 and 3 recompute the transforms
+// and velocities instead of storing them, sweep 2 re-derives V_{i-1} from V_i by
+// inverting the forward map; the only per-link scratch is Ubar = U/D and
+// ubar = u/D (7 scalars) written by sweep 2 and read by sweep 3, in a
 // slot-contiguous global workspace.  D_i <= 0 (A11) makes that state's qdd NaN.
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -23,7 +26,7 @@
 
 namespace rd {
 
-constexpr int kAbaPerLink = 17;
+constexpr int kAbaPerLink = 7;   // Ubar = U/D (6), ubar = u/D
 constexpr int kAbaThreads = 128;
 int aba_ws_per_link() { return kAbaPerLink; }
 
@@ -162,14 +165,14 @@ aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int
            T* __restrict__ qdd_out, T* __restrict__ ws, int64_t slots) {
   const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= slots) return;
+  const T zero6[6] = {0, 0, 0, 0, 0, 0};
   for (int64_t b = slot; b < B; b += slots) {
-    // ---- sweep 1: forward kinematics, velocities, c_i, bias wrenches p_i
+    // ---- sweep 1: link velocities V_i (Eq. 1), registers only; only V_n survives
     T V[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) V[k] = bnd.V0[k];
     for (int i = 0; i < n; ++i) {
       const LinkConst<T> C = L[i];
-      T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
       Rot<T> R;
       T p0, p1, p2, s, c, d;
       link_transform(C, __ldg(q + (int64_t)i * B + b), R, p0, p1, p2, s, c, d);
@@ -178,121 +181,114 @@ aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int
       ad_finv(R, p0, p1, p2, V, Vn);
       Vn[2] = fma(C.beta, qdi, Vn[2]);
       Vn[5] = fma(C.alpha, qdi, Vn[5]);
-      // c = ad_V(S qd) = qd (beta w x e_z + alpha v x e_z, alpha w x e_z)
-      const T aq = C.alpha * qdi, bq = C.beta * qdi;
-      T cc[6];
-      cc[0] = fma(bq, Vn[4], aq * Vn[1]);
-      cc[1] = -fma(bq, Vn[3], aq * Vn[0]);
-      cc[2] = 0;
-      cc[3] = aq * Vn[4];
-      cc[4] = -aq * Vn[3];
-      cc[5] = 0;
-      // p = -ad^T_V (J V): bias_force with Vdot = 0
-      const T zero6[6] = {0, 0, 0, 0, 0, 0};
-      T pb[6];
-      bias_force(C, Vn, zero6, pb);
-      w[0] = s;
-      w[slots] = c;
-      w[2 * slots] = d;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        w[(3 + k) * slots] = cc[k];
-        w[(9 + k) * slots] = pb[k];
-      }
 #pragma unroll
       for (int k = 0; k < 6; ++k) V[k] = Vn[k];
     }
-    // ---- sweep 2: articulated inertias (Eq. 7) and articulated bias forces
-    Sym6<T> K;         // Jhat_i (accumulated from the child)
-    T ph[6];           // phat_i
-    bool first = true;
-    Sym6<T> Kc;        // X_{i+1}^T Jhat^a_{i+1} X_{i+1} (child contribution)
-    T pc[6];
+    // ---- sweep 2 (backward): ABI Eq. (7) and articulated bias; V_i re-derived by
+    //      V_{i-1} = Ad_{f_i}(V_i - S_i qd_i); stores Ubar = U/D and ubar = u/D (7 per link)
+    Sym6<T> K, Kc;
+    T ph[6], pc[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) pc[k] = bnd.Ftip[k];   // F_{n+1} enters link n like a bias wrench
+#pragma unroll
+    for (int k = 0; k < 6; ++k) { Kc.a[k] = 0; Kc.c[k] = 0; }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Kc.b[k] = 0;
     for (int i = n - 1; i >= 0; --i) {
       const LinkConst<T> C = L[i];
-      T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
-      link_inertia(C, K);
+      Rot<T> R;
+      T p0, p1, p2, s, c, d;
+      link_transform(C, __ldg(q + (int64_t)i * B + b), R, p0, p1, p2, s, c, d);
+      const T qdi = __ldg(qd + (int64_t)i * B + b);
+      // c_i = ad_{V_i}(S qd) = qd (beta w x e_z + alpha v x e_z, alpha w x e_z); p_i = -ad^T_V J V
+      const T aq = C.alpha * qdi, bq = C.beta * qdi;
       T cc[6];
+      cc[0] = fma(bq, V[4], aq * V[1]);
+      cc[1] = -fma(bq, V[3], aq * V[0]);
+      cc[2] = 0;
+      cc[3] = aq * V[4];
+      cc[4] = -aq * V[3];
+      cc[5] = 0;
+      T pb[6];
+      bias_force(C, V, zero6, pb);
+      link_inertia(C, K);
 #pragma unroll
-      for (int k = 0; k < 6; ++k) { ph[k] = w[(9 + k) * slots]; cc[k] = w[(3 + k) * slots]; }
-      if (first) {
-        // F_{n+1} enters link n's balance like a bias wrench (Eq. 2: F_n = Fhat_n + F_{n+1})
+      for (int k = 0; k < 6; ++k) { K.a[k] += Kc.a[k]; K.c[k] += Kc.c[k]; ph[k] = pb[k] + pc[k]; }
 #pragma unroll
-        for (int k = 0; k < 6; ++k) ph[k] += bnd.Ftip[k];
-        first = false;
-      } else {
-#pragma unroll
-        for (int k = 0; k < 6; ++k) { K.a[k] += Kc.a[k]; K.c[k] += Kc.c[k]; ph[k] += pc[k]; }
-#pragma unroll
-        for (int k = 0; k < 9; ++k) K.b[k] += Kc.b[k];
-      }
-      // U = K S, S = (beta e_z, alpha e_z): U = beta K[:,2] + alpha K[:,5]
+      for (int k = 0; k < 9; ++k) K.b[k] += Kc.b[k];
+      // U = Jhat S, D = S^T U (= Omega), u = tau - S^T phat
       T U[6];
       {
-        T e[6] = {0, 0, C.beta, 0, 0, C.alpha};
+        const T e[6] = {0, 0, C.beta, 0, 0, C.alpha};
         sym6_mv(K, e, U);
       }
       const T D = fma(C.beta, U[2], C.alpha * U[5]);
-      const T tau_i = __ldg(tau_in + (int64_t)i * B + b);
-      const T u = tau_i - fma(C.beta, ph[2], C.alpha * ph[5]);
-      const T invD = (D > (T)0) ? (T)1 / D : (T)NAN;     // A11: per-state NaN
+      const T u = __ldg(tau_in + (int64_t)i * B + b) - fma(C.beta, ph[2], C.alpha * ph[5]);
+      const T invD = (D > (T)0) ? (T)1 / D : (T)NAN;      // A11: per-state NaN
+      const T ub = u * invD;
+      T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) w[(9 + k) * slots] = U[k];
-      w[15 * slots] = invD;
-      w[16 * slots] = u;
-      if (i == 0) break;
-      // Jhat^a = K - U U^T / D ; p^a = phat + Jhat^a c + U u / D
-      sym6_rank1_sub(K, U, invD);
-      T Kc_c[6];
-      sym6_mv(K, cc, Kc_c);
-      T pa[6];
-      const T uD = u * invD;
+      for (int k = 0; k < 6; ++k) w[k * slots] = U[k] * invD;
+      w[6 * slots] = ub;
+      if (i > 0) {
+        // Jhat^a = Jhat - U U^T / D ; p^a = phat + Jhat^a c + U u / D, moved to the parent
+        sym6_rank1_sub(K, U, invD);
+        T Kcc[6], pa[6];
+        sym6_mv(K, cc, Kcc);
 #pragma unroll
-      for (int k = 0; k < 6; ++k) pa[k] = ph[k] + Kc_c[k] + U[k] * uD;
-      // to the parent frame with X_i = Ad_{f_{i-1,i}^{-1}} of THIS link i
-      Rot<T> R;
-      T p0, p1, p2;
-      {
-        const T s = w[0], c = w[slots], d = w[2 * slots];
-        R = make_rot(C, s, c);
-        p0 = fma(d, C.Rm[2], C.pm[0]);
-        p1 = fma(d, C.Rm[5], C.pm[1]);
-        p2 = fma(d, C.Rm[8], C.pm[2]);
+        for (int k = 0; k < 6; ++k) pa[k] = ph[k] + Kcc[k] + U[k] * ub;
+        congruence(R, p0, p1, p2, K, Kc);
+        bwd_step(R, p0, p1, p2, pa, zero6, pc);
+        // V_{i-1} = Ad_{f_i}(V_i - S qd)
+        T x[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) x[k] = V[k];
+        x[2] -= bq;
+        x[5] -= aq;
+        T vr[3], wr[3];
+        rot_n(R, x[3], x[4], x[5], wr[0], wr[1], wr[2]);
+        rot_n(R, x[0], x[1], x[2], vr[0], vr[1], vr[2]);
+        V[0] = fma(p1, wr[2], fma(-p2, wr[1], vr[0]));
+        V[1] = fma(p2, wr[0], fma(-p0, wr[2], vr[1]));
+        V[2] = fma(p0, wr[1], fma(-p1, wr[0], vr[2]));
+        V[3] = wr[0]; V[4] = wr[1]; V[5] = wr[2];
       }
-      congruence(R, p0, p1, p2, K, Kc);
-      const T zero6[6] = {0, 0, 0, 0, 0, 0};
-      bwd_step(R, p0, p1, p2, pa, zero6, pc);
     }
-    // ---- sweep 3: accelerations
+    // ---- sweep 3 (forward, the role of Eq. 19): V_i and c_i again, a'_i = X_i a_{i-1} + c_i,
+    //      qdd_i = ubar_i - Ubar_i . a'_i, a_i = a'_i + S_i qdd_i
     T a[6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) a[k] = bnd.Vd0[k];
+    for (int k = 0; k < 6; ++k) { a[k] = bnd.Vd0[k]; V[k] = bnd.V0[k]; }
     for (int i = 0; i < n; ++i) {
       const LinkConst<T> C = L[i];
       const T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
+      T Ub[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) Ub[k] = w[k * slots];
+      const T ub = w[6 * slots];
       Rot<T> R;
-      T p0, p1, p2;
-      {
-        const T s = w[0], c = w[slots], d = w[2 * slots];
-        R = make_rot(C, s, c);
-        p0 = fma(d, C.Rm[2], C.pm[0]);
-        p1 = fma(d, C.Rm[5], C.pm[1]);
-        p2 = fma(d, C.Rm[8], C.pm[2]);
-      }
-      T an[6];
+      T p0, p1, p2, s, c, d;
+      link_transform(C, __ldg(q + (int64_t)i * B + b), R, p0, p1, p2, s, c, d);
+      const T qdi = __ldg(qd + (int64_t)i * B + b);
+      T Vn[6], an[6];
+      ad_finv(R, p0, p1, p2, V, Vn);
+      Vn[2] = fma(C.beta, qdi, Vn[2]);
+      Vn[5] = fma(C.alpha, qdi, Vn[5]);
       ad_finv(R, p0, p1, p2, a, an);
+      const T aq = C.alpha * qdi, bq = C.beta * qdi;
+      an[0] += fma(bq, Vn[4], aq * Vn[1]);
+      an[1] -= fma(bq, Vn[3], aq * Vn[0]);
+      an[3] += aq * Vn[4];
+      an[4] -= aq * Vn[3];
       T Ua = 0;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        an[k] += w[(3 + k) * slots];
-        Ua = fma(w[(9 + k) * slots], an[k], Ua);
-      }
-      const T qddi = (w[16 * slots] - Ua) * w[15 * slots];
+      for (int k = 0; k < 6; ++k) Ua = fma(Ub[k], an[k], Ua);
+      const T qddi = ub - Ua;
       qdd_out[(int64_t)i * B + b] = qddi;
       an[2] = fma(C.beta, qddi, an[2]);
       an[5] = fma(C.alpha, qddi, an[5]);
 #pragma unroll
-      for (int k = 0; k < 6; ++k) a[k] = an[k];
+      for (int k = 0; k < 6; ++k) { a[k] = an[k]; V[k] = Vn[k]; }
     }
   }
 }

@@ -144,6 +144,8 @@ struct rd_model_s {
   bool dh_ok = false;              // DH frames built (all revolute, zero pitch)
   std::vector<rd::LinkDH<double>> D64;
   std::vector<rd::LinkDH<float>> D32;
+  rd::LinkDH<double>* dD64 = nullptr;
+  rd::LinkDH<float>* dD32 = nullptr;
   Rigid D0;                        // DH base frame in the user's base frame
   rd::Boundary<double> bdh64;
   rd::Boundary<float> bdh32;
@@ -357,6 +359,9 @@ template <> const rd::LinkConst<float>* dev_consts<float>(rd_model_t m) { return
 template <typename T> const rd::LinkDH<T>* dh_consts(rd_model_t m);
 template <> const rd::LinkDH<double>* dh_consts<double>(rd_model_t m) { return m->D64.data(); }
 template <> const rd::LinkDH<float>* dh_consts<float>(rd_model_t m) { return m->D32.data(); }
+template <typename T> const rd::LinkDH<T>* dh_dev(rd_model_t m);
+template <> const rd::LinkDH<double>* dh_dev<double>(rd_model_t m) { return m->dD64; }
+template <> const rd::LinkDH<float>* dh_dev<float>(rd_model_t m) { return m->dD32; }
 template <typename T> const rd::Boundary<T>& dh_bnd(rd_model_t m);
 template <> const rd::Boundary<double>& dh_bnd<double>(rd_model_t m) { return m->bdh64; }
 template <> const rd::Boundary<float>& dh_bnd<float>(rd_model_t m) { return m->bdh32; }
@@ -374,13 +379,18 @@ template <> const rd::Boundary<float>& bnd<float>(rd_model_t m) { return m->b32;
 constexpr int64_t kWarpScanMaxBatch = 4096;
 
 rd_strategy_t resolve(rd_model_t m, int64_t batch, bool fp64) {
-  if (m->strategy == RD_STRAT_GENERIC) return RD_STRAT_GENERIC;
   const bool thread_ok = m->dh_ok && rd::thread_kernel_has_n(m->n, fp64);
   const bool warp_ok = m->n <= 32;
-  if (m->strategy == RD_STRAT_THREAD) return thread_ok ? RD_STRAT_THREAD : RD_STRAT_GENERIC;
-  if (m->strategy == RD_STRAT_WARP_SCAN) return warp_ok ? RD_STRAT_WARP_SCAN : RD_STRAT_GENERIC;
+  switch (m->strategy) {
+    case RD_STRAT_GENERIC: return RD_STRAT_GENERIC;
+    case RD_STRAT_THREAD: return thread_ok ? RD_STRAT_THREAD : (m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC);
+    case RD_STRAT_WARP_SCAN: return warp_ok ? RD_STRAT_WARP_SCAN : RD_STRAT_GENERIC;
+    case RD_STRAT_REVERSE: return m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
+    default: break;
+  }
   if (warp_ok && batch <= kWarpScanMaxBatch) return RD_STRAT_WARP_SCAN;
-  return thread_ok ? RD_STRAT_THREAD : RD_STRAT_GENERIC;
+  if (thread_ok) return RD_STRAT_THREAD;
+  return m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
 }
 
 template <typename T>
@@ -400,6 +410,9 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     bool ok = false;
     e = rd::launch_rnea_warp<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok);
     if (!ok) strat = RD_STRAT_GENERIC;
+  }
+  if (strat == RD_STRAT_REVERSE) {
+    e = rd::launch_rnea_rev<T>(m->n, dh_dev<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches);
   }
   if (strat == RD_STRAT_GENERIC) {
     std::lock_guard<std::mutex> lk(m->mu);
@@ -601,6 +614,12 @@ rd_status_t rd_model_create(int32_t n, const double* M, const double* S, const d
   if (e == cudaSuccess) e = cudaMalloc(&m->dL32, sizeof(rd::LinkConst<float>) * n);
   if (e == cudaSuccess) e = cudaMemcpy(m->dL64, m->L64.data(), sizeof(rd::LinkConst<double>) * n, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(m->dL32, m->L32.data(), sizeof(rd::LinkConst<float>) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && m->dh_ok) {
+    e = cudaMalloc(&m->dD64, sizeof(rd::LinkDH<double>) * n);
+    if (e == cudaSuccess) e = cudaMalloc(&m->dD32, sizeof(rd::LinkDH<float>) * n);
+    if (e == cudaSuccess) e = cudaMemcpy(m->dD64, m->D64.data(), sizeof(rd::LinkDH<double>) * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(m->dD32, m->D32.data(), sizeof(rd::LinkDH<float>) * n, cudaMemcpyHostToDevice);
+  }
   if (e != cudaSuccess) {
     rd_model_destroy(m);
     return cuda_fail(e, "model upload");
@@ -613,6 +632,8 @@ rd_status_t rd_model_destroy(rd_model_t m) {
   if (!m) return RD_OK;
   if (m->dL64) cudaFree(m->dL64);
   if (m->dL32) cudaFree(m->dL32);
+  if (m->dD64) cudaFree(m->dD64);
+  if (m->dD32) cudaFree(m->dD32);
   if (m->ws) cudaFree(m->ws);
   for (int k = 0; k < 2; ++k) {
     if (m->hbuf[k]) cudaFree(m->hbuf[k]);
@@ -626,7 +647,7 @@ int32_t rd_model_n(rd_model_t m) { return m ? m->n : -1; }
 
 rd_status_t rd_model_set_strategy(rd_model_t m, rd_strategy_t s) {
   if (!m) return fail(RD_E_ARG, "null model");
-  if (s < RD_STRAT_AUTO || s > RD_STRAT_GENERIC) return fail(RD_E_ARG, "unknown strategy");
+  if (s < RD_STRAT_AUTO || s > RD_STRAT_REVERSE) return fail(RD_E_ARG, "unknown strategy");
   m->strategy = s;
   return RD_OK;
 }

@@ -250,4 +250,19 @@ __device__ __forceinline__ void dh_bwd(T ca, T sa, T p0, T p1, T p2, T s, T c, c
   F[5] = fma(p0, y1, fma(-p1, y0, Fh[5] + z2));
 }
 
+// out = Ad_f in = (R v + p x (R w), R w), R = Rx(alpha) Rz(theta): the inverse of
+// dh_ad_finv (used to re-derive V_{i-1}, Vdot_{i-1} from V_i, Vdot_i).
+template <typename T>
+__device__ __forceinline__ void dh_ad_f(const LinkDH<T>& C, T s, T c, const T* in, T* out) {
+  // Rz y = (c y0 - s y1, s y0 + c y1, y2); Rx z = (z0, ca z1 - sa z2, sa z1 + ca z2)
+  const T a0 = fma(c, in[3], -(s * in[4])), a1 = fma(s, in[3], c * in[4]), a2 = in[5];
+  const T w0 = a0, w1 = fma(C.ca, a1, -(C.sa * a2)), w2 = fma(C.sa, a1, C.ca * a2);
+  const T b0 = fma(c, in[0], -(s * in[1])), b1 = fma(s, in[0], c * in[1]), b2 = in[2];
+  const T v0 = b0, v1 = fma(C.ca, b1, -(C.sa * b2)), v2 = fma(C.sa, b1, C.ca * b2);
+  out[0] = fma(C.p1, w2, fma(-C.p2, w1, v0));
+  out[1] = fma(C.p2, w0, fma(-C.p0, w2, v1));
+  out[2] = fma(C.p0, w1, fma(-C.p1, w0, v2));
+  out[3] = w0; out[4] = w1; out[5] = w2;
+}
+
 }  // namespace rd

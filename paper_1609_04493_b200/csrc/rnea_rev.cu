@@ -1,0 +1,135 @@
+// rnea_rev.cu -- one thread per state, serial RNEA (Eq. 1-2) with NO
+// per-link stash, for long all-revolute chains (strategy REVERSE, any n).
+//
+// The forward sweep carries only V, Vdot (Eq. 1).  The backward sweep re-derives
+// V_{i-1}, Vdot_{i-1} from V_i, Vdot_i by inverting the forward maps,
+//   V_{i-1}    = Ad_{f_i} (V_i - S_i qd_i),
+//   Vdot_{i-1} = Ad_{f_i} (Vdot_i - S_i qdd_i - ad_{V_i}(S_i qd_i)),
+// recomputes f_i (sincos) and the bias wrench Fhat_i there, and runs Eq. (2).
+// Inputs are re-read in the backward sweep (L2).  The per-state on-chip state is
+// a few dozen registers whatever n is, so the kernel keeps 16 warps per SM busy
+// where the stash kernel (rnea_thread.cu) cannot fit n links on chip.
+// Rigid transforms are well conditioned, so the re-derivation adds O(n eps)
+// relative error (GPU parity tests up to n = 200).  DH frames as in rnea_thread.
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "rd_internal.h"
+#include "rd_math.cuh"
+
+namespace rd {
+
+constexpr int kRevThreads = 128;
+
+template <typename T>
+__global__ void __launch_bounds__(kRevThreads, 4)
+rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
+                const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
+                T* __restrict__ tau) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LinkDH<T>* L = reinterpret_cast<LinkDH<T>*>(smem_raw);       // model constants, broadcast reads
+  for (int i = threadIdx.x; i < n * (int)(sizeof(LinkDH<T>) / sizeof(T)); i += blockDim.x)
+    reinterpret_cast<T*>(L)[i] = reinterpret_cast<const T*>(Lg)[i];
+  __syncthreads();
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
+    const T* pq = q + b;
+    const T* pqd = qd + b;
+    const T* pqa = qdd + b;
+    T V[6], Vd[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) { V[k] = bnd.V0[k]; Vd[k] = bnd.Vd0[k]; }
+    // ---- forward sweep, Eq. (1)
+    T nq = __ldg(pq), nqd = __ldg(pqd), nqa = __ldg(pqa);
+    for (int i = 0; i < n; ++i) {
+      const T qi = nq, qdi = nqd, qai = nqa;
+      const int64_t o = (int64_t)min(i + 1, n - 1) * B;
+      nq = __ldg(pq + o); nqd = __ldg(pqd + o); nqa = __ldg(pqa + o);
+      const LinkDH<T> C = L[i];
+      T s, c;
+      if (sizeof(T) == 8) {
+        rd_sincos(qi + C.th0, &s, &c);
+      } else {
+        T s0, c0;
+        rd_sincos(qi, &s0, &c0);
+        s = fma(s0, C.cth0, c0 * C.sth0);
+        c = fma(c0, C.cth0, -(s0 * C.sth0));
+      }
+      T Vn[6], Vdn[6];
+      dh_ad_finv(C, s, c, V, Vn);
+      dh_ad_finv(C, s, c, Vd, Vdn);
+      Vn[5] += qdi;
+      Vdn[5] += qai;
+      Vdn[0] = fma(qdi, Vn[1], Vdn[0]);
+      Vdn[1] = fma(-qdi, Vn[0], Vdn[1]);
+      Vdn[3] = fma(qdi, Vn[4], Vdn[3]);
+      Vdn[4] = fma(-qdi, Vn[3], Vdn[4]);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) { V[k] = Vn[k]; Vd[k] = Vdn[k]; }
+    }
+    // ---- backward sweep, Eq. (2), re-deriving V, Vdot link by link
+    T F[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) F[k] = bnd.Ftip[k];
+    T ca = 1, sa = 0, p0 = 0, p1 = 0, p2 = 0, sn = 0, cn = 1;   // child transform (identity at the tip)
+    const int64_t on = (int64_t)(n - 1) * B;
+    nq = __ldg(pq + on); nqd = __ldg(pqd + on); nqa = __ldg(pqa + on);
+    for (int i = n - 1; i >= 0; --i) {
+      const T qi = nq, qdi = nqd, qai = nqa;
+      const int64_t o = (int64_t)max(i - 1, 0) * B;
+      nq = __ldg(pq + o); nqd = __ldg(pqd + o); nqa = __ldg(pqa + o);
+      const LinkDH<T> C = L[i];
+      T Fh[6], Fo[6];
+      bias_force(C, V, Vd, Fh);
+      dh_bwd(ca, sa, p0, p1, p2, sn, cn, F, Fh, Fo);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) F[k] = Fo[k];
+      tau[(int64_t)i * B + b] = F[5];
+      T s, c;
+      if (sizeof(T) == 8) {
+        rd_sincos(qi + C.th0, &s, &c);
+      } else {
+        T s0, c0;
+        rd_sincos(qi, &s0, &c0);
+        s = fma(s0, C.cth0, c0 * C.sth0);
+        c = fma(c0, C.cth0, -(s0 * C.sth0));
+      }
+      // V_{i-1}, Vdot_{i-1}
+      T x[6], y[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) { x[k] = V[k]; y[k] = Vd[k]; }
+      x[5] -= qdi;
+      y[5] -= qai;
+      y[0] = fma(-qdi, V[1], y[0]);
+      y[1] = fma(qdi, V[0], y[1]);
+      y[3] = fma(-qdi, V[4], y[3]);
+      y[4] = fma(qdi, V[3], y[4]);
+      dh_ad_f(C, s, c, x, V);
+      dh_ad_f(C, s, c, y, Vd);
+      ca = C.ca; sa = C.sa; p0 = C.p0; p1 = C.p1; p2 = C.p2; sn = s; cn = c;
+    }
+  }
+}
+
+template <typename T>
+cudaError_t launch_rnea_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
+                            const T* qd, const T* qdd, T* tau, cudaStream_t st, int* launches) {
+  const size_t smem = (size_t)n * sizeof(LinkDH<T>);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(rnea_rev_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  int64_t grid = (B + kRevThreads - 1) / kRevThreads;
+  const int64_t cap = (int64_t)num_sms() * 4;
+  if (grid > cap) grid = cap;
+  rnea_rev_kernel<T><<<(unsigned)grid, kRevThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_rnea_rev<double>(int, const LinkDH<double>*, const Boundary<double>&, int64_t,
+                                             const double*, const double*, const double*, double*, cudaStream_t,
+                                             int*);
+template cudaError_t launch_rnea_rev<float>(int, const LinkDH<float>*, const Boundary<float>&, int64_t,
+                                            const float*, const float*, const float*, float*, cudaStream_t, int*);
+
+}  // namespace rd

@@ -80,7 +80,7 @@ def test_C3_full_size_sampled(rd, dtype):
     check_id(rd, synth.robot_for(cfg), cfg["gravity"], q, qd, qdd, dtype, sample=sample)
 
 
-@pytest.mark.parametrize("strategy", ["thread", "generic", "warp_scan"])
+@pytest.mark.parametrize("strategy", ["thread", "generic", "warp_scan", "reverse"])
 def test_C3_small_all_states(rd, strategy):
     cfg = synth.CONFIGS["C3"]
     q, qd, qdd = synth.states(cfg["seed"], 30, 0, 3000, cfg["ranges"])
@@ -92,7 +92,7 @@ def test_C3_small_all_states(rd, strategy):
 def test_ragged_batches(rd, B):
     r = synth.random_chain(30, 1030)
     q, qd, qdd = synth.states(7, 30, 0, B)
-    for strat in ("auto", "thread", "warp_scan", "generic"):
+    for strat in ("auto", "thread", "warp_scan", "generic", "reverse"):
         check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strat)
 
 
@@ -102,11 +102,11 @@ def test_empty_batch_is_noop(rd):
     rd.inverse_dynamics(model, z, z, z, out=torch.empty((6, 0), dtype=torch.float64, device="cuda"))
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 6, 7, 10, 13, 30, 64, 100])
+@pytest.mark.parametrize("n", [1, 2, 3, 6, 7, 10, 13, 30, 31, 32, 33, 64, 100, 200])
 def test_link_counts_random_chains(rd, n):
     r = synth.random_chain(n, 500 + n)
     q, qd, qdd = synth.states(11, n, 0, 777)
-    for strat in ("auto", "generic") + (("warp_scan",) if n <= 32 else ()):
+    for strat in ("auto", "generic", "reverse", "thread") + (("warp_scan",) if n <= 32 else ()):
         check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strat)
 
 
@@ -148,7 +148,7 @@ def test_full_boundary_V0_Vdot0_Ftip(rd):
     r2 = synth.random_chain(7, 32)                 # all revolute -> thread kernel
     model2 = rd.Model.from_robot(r2, (0, 0, 0))
     model2.set_boundary(V0, Vd0, Ft)
-    for strat in ("thread", "generic", "warp_scan"):
+    for strat in ("thread", "generic", "warp_scan", "reverse"):
         model2.set_strategy(strat)
         tau = rd.inverse_dynamics(model2, dev(q), dev(qd), dev(qdd)).cpu().numpy()
         ref = np.stack([oracle.rnea(r2, q[:, b], qd[:, b], qdd[:, b], V0, Vd0, Ft) for b in range(300)], 1)
@@ -159,7 +159,7 @@ def test_deterministic_and_strategy_consistent(rd):
     cfg = synth.CONFIGS["C3"]
     q, qd, qdd = synth.states(cfg["seed"], 30, 0, 20000)
     model = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
-    for strat in ("thread", "warp_scan", "generic"):
+    for strat in ("thread", "warp_scan", "generic", "reverse"):
         # with a FIXED strategy, results are bit-identical across repeats and across sharding
         # (AUTO picks the strategy from the per-call batch size)
         model.set_strategy(strat)
@@ -274,7 +274,7 @@ def test_large_joint_angles(rd, dtype, scale):
     r = synth.random_chain(30, 1030)
     q, qd, qdd = synth.states(21, 30, 0, 5000)
     q = q / np.pi * scale
-    for strat in ("thread", "generic", "warp_scan"):
+    for strat in ("thread", "generic", "warp_scan", "reverse"):
         check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype, strategy=strat)
 
 
