@@ -1,0 +1,2 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu 2>&1 | grep -E "FAILED|Error|assert|passed|failed" | head -20
+for i in 1 2; do timeout 300 python tools/quick_time.py 2>&1 | grep -E "C3 float(64|32) thread|C2 float(64|32) thread"; done
