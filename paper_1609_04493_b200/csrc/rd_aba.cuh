@@ -1,0 +1,138 @@
+// rd_aba.cuh -- articulated-body helpers shared by the ABA kernels (product path):
+// symmetric 6x6 spatial inertias in 3x3 blocks, the congruence X^T K X for
+// X = Ad_{f^-1}, the link inertia and transform in joint frames.
+#pragma once
+#include "rd_internal.h"
+#include "rd_math.cuh"
+
+namespace rd {
+
+// Symmetric 6x6 K = [[A, B], [B^T, C]]: A, C symmetric (xx yy zz xy xz yz), B general row-major.
+template <typename T>
+struct Sym6 {
+  T a[6], b[9], c[6];
+};
+
+// y = K x
+template <typename T>
+__device__ __forceinline__ void sym6_mv(const Sym6<T>& K, const T* x, T* y) {
+  const T* A = K.a;
+  const T* Bm = K.b;
+  const T* C = K.c;
+  y[0] = A[0] * x[0] + A[3] * x[1] + A[4] * x[2] + Bm[0] * x[3] + Bm[1] * x[4] + Bm[2] * x[5];
+  y[1] = A[3] * x[0] + A[1] * x[1] + A[5] * x[2] + Bm[3] * x[3] + Bm[4] * x[4] + Bm[5] * x[5];
+  y[2] = A[4] * x[0] + A[5] * x[1] + A[2] * x[2] + Bm[6] * x[3] + Bm[7] * x[4] + Bm[8] * x[5];
+  y[3] = Bm[0] * x[0] + Bm[3] * x[1] + Bm[6] * x[2] + C[0] * x[3] + C[3] * x[4] + C[4] * x[5];
+  y[4] = Bm[1] * x[0] + Bm[4] * x[1] + Bm[7] * x[2] + C[3] * x[3] + C[1] * x[4] + C[5] * x[5];
+  y[5] = Bm[2] * x[0] + Bm[5] * x[1] + Bm[8] * x[2] + C[4] * x[3] + C[5] * x[4] + C[2] * x[5];
+}
+
+// K -= u u^T / D
+template <typename T>
+__device__ __forceinline__ void sym6_rank1_sub(Sym6<T>& K, const T* u, T invD) {
+  T w[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) w[k] = u[k] * invD;
+  K.a[0] -= w[0] * u[0]; K.a[1] -= w[1] * u[1]; K.a[2] -= w[2] * u[2];
+  K.a[3] -= w[0] * u[1]; K.a[4] -= w[0] * u[2]; K.a[5] -= w[1] * u[2];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) K.b[3 * i + j] -= w[i] * u[3 + j];
+  K.c[0] -= w[3] * u[3]; K.c[1] -= w[4] * u[4]; K.c[2] -= w[5] * u[5];
+  K.c[3] -= w[3] * u[4]; K.c[4] -= w[3] * u[5]; K.c[5] -= w[4] * u[5];
+}
+
+// Full 3x3 from symmetric storage.
+template <typename T>
+__device__ __forceinline__ void sym_full(const T* s, T* M) {
+  M[0] = s[0]; M[1] = s[3]; M[2] = s[4];
+  M[3] = s[3]; M[4] = s[1]; M[5] = s[5];
+  M[6] = s[4]; M[7] = s[5]; M[8] = s[2];
+}
+
+// out = R M R^T (M general 3x3 row-major)
+template <typename T>
+__device__ __forceinline__ void rot_conj(const Rot<T>& R, const T* M, T* out) {
+  const T r[9] = {R.r00, R.r01, R.r02, R.r10, R.r11, R.r12, R.r20, R.r21, R.r22};
+  T t[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) t[3 * i + j] = r[3 * i] * M[j] + r[3 * i + 1] * M[3 + j] + r[3 * i + 2] * M[6 + j];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) out[3 * i + j] = t[3 * i] * r[3 * j] + t[3 * i + 1] * r[3 * j + 1] + t[3 * i + 2] * r[3 * j + 2];
+}
+
+// Congruence X^T K X with X = Ad_{f^-1}, f = (R, p) (derivation in DESIGN.md):
+//   A' = R A R^T, B' = R B R^T, C' = R C R^T, P = [p]
+//   A_new = A',  B_new = B' - A' P,  C_new = C' + P B' + (P B')^T - P A' P.
+template <typename T>
+__device__ __forceinline__ void congruence(const Rot<T>& R, T p0, T p1, T p2, const Sym6<T>& K, Sym6<T>& out) {
+  T Af[9], Cf[9], Ap[9], Bp[9], Cp[9];
+  sym_full(K.a, Af);
+  sym_full(K.c, Cf);
+  rot_conj(R, Af, Ap);
+  rot_conj(R, K.b, Bp);
+  rot_conj(R, Cf, Cp);
+  // A'P: column j = A' (p x e_j); p x e_0 = (0, p2, -p1), p x e_1 = (-p2, 0, p0), p x e_2 = (p1, -p0, 0)
+  T AP[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    AP[3 * i + 0] = Ap[3 * i + 1] * p2 - Ap[3 * i + 2] * p1;
+    AP[3 * i + 1] = Ap[3 * i + 2] * p0 - Ap[3 * i + 0] * p2;
+    AP[3 * i + 2] = Ap[3 * i + 0] * p1 - Ap[3 * i + 1] * p0;
+  }
+  // P X for a 3x3 X: column j = p x X[:, j]
+  T PB[9], PAP[9];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const T x0 = Bp[j], x1 = Bp[3 + j], x2 = Bp[6 + j];
+    PB[j] = p1 * x2 - p2 * x1;
+    PB[3 + j] = p2 * x0 - p0 * x2;
+    PB[6 + j] = p0 * x1 - p1 * x0;
+    const T y0 = AP[j], y1 = AP[3 + j], y2 = AP[6 + j];
+    PAP[j] = p1 * y2 - p2 * y1;
+    PAP[3 + j] = p2 * y0 - p0 * y2;
+    PAP[6 + j] = p0 * y1 - p1 * y0;
+  }
+  out.a[0] = Ap[0]; out.a[1] = Ap[4]; out.a[2] = Ap[8];
+  out.a[3] = Ap[1]; out.a[4] = Ap[2]; out.a[5] = Ap[5];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) out.b[k] = Bp[k] - AP[k];
+  // C_new(i,j) = C'(i,j) + PB(i,j) + PB(j,i) - PAP(i,j)   (symmetric)
+  out.c[0] = Cp[0] + 2 * PB[0] - PAP[0];
+  out.c[1] = Cp[4] + 2 * PB[4] - PAP[4];
+  out.c[2] = Cp[8] + 2 * PB[8] - PAP[8];
+  out.c[3] = Cp[1] + PB[1] + PB[3] - PAP[1];
+  out.c[4] = Cp[2] + PB[2] + PB[6] - PAP[2];
+  out.c[5] = Cp[5] + PB[5] + PB[7] - PAP[5];
+}
+
+template <typename T>
+__device__ __forceinline__ void link_inertia(const LinkConst<T>& C, Sym6<T>& K) {
+  // J = [[m I, -[h]], [[h], I]]
+  K.a[0] = C.m; K.a[1] = C.m; K.a[2] = C.m; K.a[3] = 0; K.a[4] = 0; K.a[5] = 0;
+  const T h0 = C.h[0], h1 = C.h[1], h2 = C.h[2];
+  // -[h] = [[0, h2, -h1], [-h2, 0, h0], [h1, -h0, 0]]
+  K.b[0] = 0;   K.b[1] = h2;  K.b[2] = -h1;
+  K.b[3] = -h2; K.b[4] = 0;   K.b[5] = h0;
+  K.b[6] = h1;  K.b[7] = -h0; K.b[8] = 0;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) K.c[k] = C.I[k];
+}
+
+template <typename T>
+__device__ __forceinline__ void link_transform(const LinkConst<T>& C, T qi, Rot<T>& R, T& p0, T& p1, T& p2,
+                                               T& s, T& c, T& d) {
+  rd_sincos(C.alpha * qi, &s, &c);
+  d = C.beta * qi;
+  R = make_rot(C, s, c);
+  p0 = fma(d, C.Rm[2], C.pm[0]);
+  p1 = fma(d, C.Rm[5], C.pm[1]);
+  p2 = fma(d, C.Rm[8], C.pm[2]);
+}
+
+}  // namespace rd

@@ -67,7 +67,7 @@ rnea_warp_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> b
     if (act) {
       qi = __ldg(q + (int64_t)lane * B + b);
       qdi = __ldg(qd + (int64_t)lane * B + b);
-      qddi = __ldg(qdd + (int64_t)lane * B + b);
+      qddi = qdd ? __ldg(qdd + (int64_t)lane * B + b) : T(0);   // qdd == nullptr: qdd = 0 (tau_bias, Eq. 5)
     }
     // CalcTransform: f_l = (Rm Rz(alpha q), pm + beta q Rm e_z)
     T s, cc;

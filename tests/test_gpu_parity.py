@@ -319,3 +319,21 @@ def test_fd_jsiia_boundary_and_limits(rd):
     z = torch.zeros((40, 10), dtype=torch.float64, device="cuda")
     with pytest.raises(rd.RdError):
         rd.forward_dynamics(big, z, z, z)
+
+
+# ------------------------------------------------------------------ forward dynamics (scan ABIA, Alg. 3)
+@pytest.mark.parametrize("n,pf", [(1, 0.0), (2, 0.0), (7, 0.3), (16, 0.0), (30, 0.0), (32, 0.2)])
+def test_fd_aba_scan_parity(rd, n, pf):
+    r = synth.random_chain(n, 800 + n, prismatic_fraction=pf)
+    g = synth.GRAVITY_Z
+    q, qd, qdd = synth.states(19, n, 0, 1500)
+    tau = oracle.rnea_batch(r, g, q, qd, qdd)
+    model = rd.Model.from_robot(r, g)
+    model.set_fd_algo("aba_scan")
+    out = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()
+    assert np.all(np.isfinite(out))
+    back = oracle.rnea_batch(r, g, q, qd, out)
+    assert rel_err_per_state(back, tau).max() <= 1e-10
+    ref = oracle.fd_batch(r, g, q, qd, tau)
+    assert rel_err_per_state(out, ref, floor=1.0).max() < 1e-7
+    assert rd.last_launch_count() == 3

@@ -81,7 +81,7 @@ def main():
                 continue
             q, qd, qdd = rnd(n, B, -np.pi, np.pi), rnd(n, B, -1, 1), rnd(n, B, -1, 1)
             out = torch.empty_like(q)
-            for strat in ("thread", "warp_scan", "generic", "auto"):
+            for strat in ("thread", "warp_scan", "reverse", "generic", "auto"):
                 model.set_strategy(strat)
                 used = model.resolve_strategy(B, dt == torch.float64)
                 if strat != "auto" and used != strat:
@@ -102,8 +102,8 @@ def main():
             model.set_fd_algo("aba")
             tau = rd.inverse_dynamics(model, q, qd, qdd)
             out = torch.empty_like(q)
-            for algo in ("aba", "jsiia"):
-                if algo == "jsiia" and n > 31:
+            for algo in ("aba", "jsiia", "aba_scan"):
+                if (algo == "jsiia" and n > 31) or (algo == "aba_scan" and n > 32):
                     continue
                 model.set_fd_algo(algo)
                 ms = time_call(lambda: rd.forward_dynamics(model, q, qd, tau, out), 10)
