@@ -56,8 +56,10 @@ typedef enum {
   RD_STRAT_THREAD = 1,    /* one thread per state, serial recursion (stash in TMEM/registers) */
   RD_STRAT_WARP_SCAN = 2, /* one warp per state, lane = link, Kogge-Stone shuffle scans */
   RD_STRAT_GENERIC = 3,   /* one thread per state, any n, any joints, stash in a global workspace */
-  RD_STRAT_REVERSE = 4    /* one thread per state, any n (all-revolute chains), no stash: the backward
+  RD_STRAT_REVERSE = 4,   /* one thread per state, any n (all-revolute chains), no stash: the backward
                              sweep re-derives V, Vdot by inverting the forward maps */
+  RD_STRAT_BLOCK_SCAN = 5 /* one CTA per state, thread = link, CTA-wide scans: the single-robot latency
+                             mode for long chains (n <= 512) */
 } rd_strategy_t;
 
 /* Forward-dynamics algorithm. */

@@ -376,7 +376,11 @@ template <> const rd::Boundary<float>& bnd<float>(rd_model_t m) { return m->b32;
 //  * otherwise THREAD when the on-chip stash fits (n <= 30 fp64 / 32 fp32, all
 //    joints revolute with zero pitch): 3.9x faster than WARP_SCAN at B = 1M;
 //  * otherwise GENERIC (any n, any joint type).
+//  * 32 < n <= 512 and batch <= kBlockScanMaxBatch -> BLOCK_SCAN: one CTA per
+//    state (NEXT-3), e.g. n = 512, B = 1: 29 us vs 262 us (REVERSE), 687 us (GENERIC);
+//  * longer all-revolute chains at larger batch -> REVERSE (stash-free), else GENERIC.
 constexpr int64_t kWarpScanMaxBatch = 4096;
+constexpr int64_t kBlockScanMaxBatch = 1024;
 
 rd_strategy_t resolve(rd_model_t m, int64_t batch, bool fp64) {
   const bool thread_ok = m->dh_ok && rd::thread_kernel_has_n(m->n, fp64);
@@ -386,9 +390,11 @@ rd_strategy_t resolve(rd_model_t m, int64_t batch, bool fp64) {
     case RD_STRAT_THREAD: return thread_ok ? RD_STRAT_THREAD : (m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC);
     case RD_STRAT_WARP_SCAN: return warp_ok ? RD_STRAT_WARP_SCAN : RD_STRAT_GENERIC;
     case RD_STRAT_REVERSE: return m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
+    case RD_STRAT_BLOCK_SCAN: return m->n <= 512 ? RD_STRAT_BLOCK_SCAN : RD_STRAT_GENERIC;
     default: break;
   }
   if (warp_ok && batch <= kWarpScanMaxBatch) return RD_STRAT_WARP_SCAN;
+  if (!warp_ok && m->n <= 512 && batch <= kBlockScanMaxBatch) return RD_STRAT_BLOCK_SCAN;
   if (thread_ok) return RD_STRAT_THREAD;
   return m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
 }
@@ -409,6 +415,11 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   } else if (strat == RD_STRAT_WARP_SCAN) {
     bool ok = false;
     e = rd::launch_rnea_warp<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok);
+    if (!ok) strat = RD_STRAT_GENERIC;
+  }
+  if (strat == RD_STRAT_BLOCK_SCAN) {
+    bool ok = false;
+    e = rd::launch_rnea_block<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok);
     if (!ok) strat = RD_STRAT_GENERIC;
   }
   if (strat == RD_STRAT_REVERSE) {
@@ -657,7 +668,7 @@ int32_t rd_model_n(rd_model_t m) { return m ? m->n : -1; }
 
 rd_status_t rd_model_set_strategy(rd_model_t m, rd_strategy_t s) {
   if (!m) return fail(RD_E_ARG, "null model");
-  if (s < RD_STRAT_AUTO || s > RD_STRAT_REVERSE) return fail(RD_E_ARG, "unknown strategy");
+  if (s < RD_STRAT_AUTO || s > RD_STRAT_BLOCK_SCAN) return fail(RD_E_ARG, "unknown strategy");
   m->strategy = s;
   return RD_OK;
 }

@@ -106,7 +106,7 @@ def test_empty_batch_is_noop(rd):
 def test_link_counts_random_chains(rd, n):
     r = synth.random_chain(n, 500 + n)
     q, qd, qdd = synth.states(11, n, 0, 777)
-    for strat in ("auto", "generic", "reverse", "thread") + (("warp_scan",) if n <= 32 else ()):
+    for strat in ("auto", "generic", "reverse", "thread", "block_scan") + (("warp_scan",) if n <= 32 else ()):
         check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strat)
 
 
@@ -337,3 +337,12 @@ def test_fd_aba_scan_parity(rd, n, pf):
     ref = oracle.fd_batch(r, g, q, qd, tau)
     assert rel_err_per_state(out, ref, floor=1.0).max() < 1e-7
     assert rd.last_launch_count() == 3
+
+
+@pytest.mark.parametrize("n", [33, 100, 257, 512])
+def test_block_scan_long_chains(rd, n):
+    # NEXT-3 single-robot latency mode: one CTA per state, CTA-wide scans
+    r = synth.random_chain(n, 600 + n, prismatic_fraction=0.1)
+    q, qd, qdd = synth.states(23, n, 0, 64)
+    check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy="block_scan")
+    check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, torch.float32, strategy="block_scan")
