@@ -1,0 +1,32 @@
+"""Small invocations of every kernel for compute-sanitizer (memcheck / racecheck /
+synccheck / initcheck).  Each strategy / FD algorithm on small ragged batches."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+import paper_1609_04493_b200 as rd  # noqa: E402
+
+for dt in (torch.float64, torch.float32):
+    for n, pf in ((7, 0.0), (30, 0.0), (12, 0.4), (40, 0.0)):
+        robot = synth.random_chain(n, 50 + n, prismatic_fraction=pf)
+        model = rd.Model.from_robot(robot, synth.GRAVITY_Z)
+        for B in (1, 37, 300):
+            q, qd, qdd = (torch.from_numpy(x).to("cuda", dt) for x in synth.states(1, n, 0, B))
+            skip = os.environ.get("SKIP_STRATS", "").split(",")
+            for strat in ("thread", "warp_scan", "generic", "reverse", "block_scan"):
+                if strat in skip:
+                    continue
+                model.set_strategy(strat)
+                rd.inverse_dynamics(model, q, qd, qdd)
+            tau = rd.inverse_dynamics(model, q, qd, qdd)
+            for algo in ("aba", "jsiia", "aba_scan"):
+                if (algo == "jsiia" and n > 31) or (algo == "aba_scan" and n > 32):
+                    continue
+                model.set_fd_algo(algo)
+                rd.forward_dynamics(model, q, qd, tau)
+torch.cuda.synchronize()
+print("sanitize_run ok")
