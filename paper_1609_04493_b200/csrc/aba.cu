@@ -21,6 +21,7 @@
 // slot-contiguous global workspace.  D_i <= 0 (A11) makes that state's qdd NaN.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include "rd_internal.h"
 #include "rd_math.cuh"
 #include "rd_aba.cuh"
@@ -165,6 +166,128 @@ aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int
     }
   }
 }
+
+// ---------------------------------------------------------------- DH-frame variant
+// All-revolute chains in DH frames (the THREAD ID kernel's frames): same three
+// sweeps, with the plane-rotation congruence (dh_congruence) and the 22-flop
+// Ad maps; S = (0, e_z) so U = Jhat[:, 5], D = U[5], u = tau - phat[5].
+template <typename T, int MB>
+__global__ void __launch_bounds__(kAbaThreads, MB)
+aba_dh_kernel(int n, const LinkDH<T>* __restrict__ L, const Boundary<T> bnd, int64_t B,
+              const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ tau_in,
+              T* __restrict__ qdd_out, T* __restrict__ ws, int64_t slots) {
+  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= slots) return;
+  const T zero6[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t b = slot; b < B; b += slots) {
+    T V[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) V[k] = bnd.V0[k];
+    for (int i = 0; i < n; ++i) {                 // sweep 1: V_n
+      const LinkDH<T> C = L[i];
+      T s, c;
+      dh_sincos(C, __ldg(q + (int64_t)i * B + b), &s, &c);
+      T Vn[6];
+      dh_ad_finv(C, s, c, V, Vn);
+      Vn[5] += __ldg(qd + (int64_t)i * B + b);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) V[k] = Vn[k];
+    }
+    Sym6<T> K, Kc;
+    T pc[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) { pc[k] = bnd.Ftip[k]; Kc.a[k] = 0; Kc.c[k] = 0; }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Kc.b[k] = 0;
+    for (int i = n - 1; i >= 0; --i) {            // sweep 2
+      const LinkDH<T> C = L[i];
+      T s, c;
+      dh_sincos(C, __ldg(q + (int64_t)i * B + b), &s, &c);
+      const T qdi = __ldg(qd + (int64_t)i * B + b);
+      T cc[6] = {qdi * V[1], -qdi * V[0], 0, qdi * V[4], -qdi * V[3], 0};   // ad_V(e_z qd)
+      T ph[6];
+      bias_force(C, V, zero6, ph);
+      dh_inertia(C, K);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) { K.a[k] += Kc.a[k]; K.c[k] += Kc.c[k]; ph[k] += pc[k]; }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) K.b[k] += Kc.b[k];
+      // U = K e_5 = (B[:, 2], C[:, 2])
+      T U[6] = {K.b[2], K.b[5], K.b[8], K.c[4], K.c[5], K.c[2]};
+      const T D = U[5];
+      const T invD = (D > (T)0) ? (T)1 / D : (T)NAN;
+      const T ub = (__ldg(tau_in + (int64_t)i * B + b) - ph[5]) * invD;
+      T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) w[k * slots] = U[k] * invD;
+      w[6 * slots] = ub;
+      if (i > 0) {
+        sym6_rank1_sub(K, U, invD);
+        T Kcc[6], pa[6];
+        sym6_mv(K, cc, Kcc);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) pa[k] = ph[k] + Kcc[k] + U[k] * ub;
+        Kc = K;
+        dh_congruence(C, s, c, Kc);
+        dh_bwd(C.ca, C.sa, C.p0, C.p1, C.p2, s, c, pa, zero6, pc);
+        T x[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) x[k] = V[k];
+        x[5] -= qdi;
+        dh_ad_f(C, s, c, x, V);                    // V_{i-1} = Ad_{f_i}(V_i - S qd)
+      }
+    }
+    T a[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) { a[k] = bnd.Vd0[k]; V[k] = bnd.V0[k]; }
+    for (int i = 0; i < n; ++i) {                 // sweep 3
+      const LinkDH<T> C = L[i];
+      const T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
+      T Ub[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) Ub[k] = w[k * slots];
+      const T ub = w[6 * slots];
+      T s, c;
+      dh_sincos(C, __ldg(q + (int64_t)i * B + b), &s, &c);
+      const T qdi = __ldg(qd + (int64_t)i * B + b);
+      T Vn[6], an[6];
+      dh_ad_finv(C, s, c, V, Vn);
+      Vn[5] += qdi;
+      dh_ad_finv(C, s, c, a, an);
+      an[0] = fma(qdi, Vn[1], an[0]);
+      an[1] = fma(-qdi, Vn[0], an[1]);
+      an[3] = fma(qdi, Vn[4], an[3]);
+      an[4] = fma(-qdi, Vn[3], an[4]);
+      T Ua = 0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) Ua = fma(Ub[k], an[k], Ua);
+      const T qddi = ub - Ua;
+      qdd_out[(int64_t)i * B + b] = qddi;
+      an[5] += qddi;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) { a[k] = an[k]; V[k] = Vn[k]; }
+    }
+  }
+}
+
+template <typename T>
+cudaError_t launch_aba_dh(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
+                          const T* qd, const T* tau, T* qdd, T* ws, int64_t ws_slots, cudaStream_t st,
+                          int* launches) {
+  const int64_t grid = (ws_slots + kAbaThreads - 1) / kAbaThreads;
+  static const int mb = getenv("RD_ABA_MB") ? atoi(getenv("RD_ABA_MB")) : 3;   // A/B knob (occupancy)
+  if (mb == 2) aba_dh_kernel<T, 2><<<(unsigned)grid, kAbaThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots);
+  else if (mb == 4) aba_dh_kernel<T, 4><<<(unsigned)grid, kAbaThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots);
+  else aba_dh_kernel<T, 3><<<(unsigned)grid, kAbaThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots);
+  ++*launches;
+  return cudaGetLastError();
+}
+template cudaError_t launch_aba_dh<double>(int, const LinkDH<double>*, const Boundary<double>&, int64_t,
+                                           const double*, const double*, const double*, double*, double*, int64_t,
+                                           cudaStream_t, int*);
+template cudaError_t launch_aba_dh<float>(int, const LinkDH<float>*, const Boundary<float>&, int64_t,
+                                          const float*, const float*, const float*, float*, float*, int64_t,
+                                          cudaStream_t, int*);
 
 template <typename T>
 cudaError_t launch_aba(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,

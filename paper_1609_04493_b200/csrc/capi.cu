@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -466,8 +467,12 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   const int64_t slots = rd::generic_ws_slots(batch);
   st = ensure_ws(m, (size_t)slots * m->n * rd::aba_ws_per_link() * sizeof(T));
   if (st != RD_OK) return st;
-  cudaError_t e = rd::launch_aba<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
-                                    reinterpret_cast<T*>(m->ws), slots, s, &g_launches);
+  static const bool no_dh = getenv("RD_ABA_NODH") && getenv("RD_ABA_NODH")[0] == '1';   // A/B knob
+  cudaError_t e = (m->dh_ok && !no_dh)
+      ? rd::launch_aba_dh<T>(m->n, dh_dev<T>(m), dh_bnd<T>(m), batch, q, qd, tau, qdd,
+                             reinterpret_cast<T*>(m->ws), slots, s, &g_launches)
+      : rd::launch_aba<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
+                          reinterpret_cast<T*>(m->ws), slots, s, &g_launches);
   if (e != cudaSuccess) return cuda_fail(e, "forward dynamics launch");
   return RD_OK;
 }

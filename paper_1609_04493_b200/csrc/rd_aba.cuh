@@ -136,3 +136,105 @@ __device__ __forceinline__ void link_transform(const LinkConst<T>& C, T qi, Rot<
 }
 
 }  // namespace rd
+
+namespace rd {
+
+// ---------------------------------------------------------------- DH-frame congruence
+// X^T K X for X = Ad_{f^-1}, f = (Rx(alpha) Rz(theta), p): rotate the blocks by
+// Rz(theta), then by Rx(alpha) (each a plane rotation: ~14 flops per symmetric
+// block, 24 per general block), then the p-shift of congruence() above.
+template <typename T>
+__device__ __forceinline__ void sym_rot_plane(T* a, int i, int j, int k, T c, T s) {
+  // symmetric block in (xx yy zz xy xz yz) storage; rotate the (i, j) plane, k the fixed axis
+  auto idx = [](int r, int q) { return r == q ? r : 2 + r + q; };   // (0,1)->3 (0,2)->4 (1,2)->5
+  const T aii = a[idx(i, i)], ajj = a[idx(j, j)], aij = a[idx(i, j)], aik = a[idx(i, k)], ajk = a[idx(j, k)];
+  const T cc = c * c, ss = s * s, cs = c * s;
+  a[idx(i, i)] = fma(cc, aii, fma(-2 * cs, aij, ss * ajj));
+  a[idx(j, j)] = fma(ss, aii, fma(2 * cs, aij, cc * ajj));
+  a[idx(i, j)] = fma(cs, aii - ajj, (cc - ss) * aij);
+  a[idx(i, k)] = fma(c, aik, -(s * ajk));
+  a[idx(j, k)] = fma(s, aik, c * ajk);
+}
+template <typename T>
+__device__ __forceinline__ void gen_rot_plane(T* b, int i, int j, T c, T s) {
+  // B <- R B R^T for the plane rotation R of the (i, j) plane (B general 3x3, row-major)
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {                  // rows i, j
+    const T bi = b[3 * i + q], bj = b[3 * j + q];
+    b[3 * i + q] = fma(c, bi, -(s * bj));
+    b[3 * j + q] = fma(s, bi, c * bj);
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {                  // columns i, j
+    const T bi = b[3 * r + i], bj = b[3 * r + j];
+    b[3 * r + i] = fma(c, bi, -(s * bj));
+    b[3 * r + j] = fma(s, bi, c * bj);
+  }
+}
+template <typename T>
+__device__ __forceinline__ void dh_congruence(const LinkDH<T>& C, T s, T c, Sym6<T>& K) {
+  // Rz(theta): plane (0, 1), fixed axis 2
+  sym_rot_plane(K.a, 0, 1, 2, c, s);
+  gen_rot_plane(K.b, 0, 1, c, s);
+  sym_rot_plane(K.c, 0, 1, 2, c, s);
+  // Rx(alpha): plane (1, 2), fixed axis 0
+  sym_rot_plane(K.a, 1, 2, 0, C.ca, C.sa);
+  gen_rot_plane(K.b, 1, 2, C.ca, C.sa);
+  sym_rot_plane(K.c, 1, 2, 0, C.ca, C.sa);
+  // p-shift: B_new = B' - A'[p], C_new = C' + [p]B' + ([p]B')^T - [p]A'[p]
+  const T p0 = C.p0, p1 = C.p1, p2 = C.p2;
+  T Ap[9];
+  sym_full(K.a, Ap);
+  T AP[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    AP[3 * i + 0] = Ap[3 * i + 1] * p2 - Ap[3 * i + 2] * p1;
+    AP[3 * i + 1] = Ap[3 * i + 2] * p0 - Ap[3 * i + 0] * p2;
+    AP[3 * i + 2] = Ap[3 * i + 0] * p1 - Ap[3 * i + 1] * p0;
+  }
+  T PB[9], PAP[9];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const T x0 = K.b[j], x1 = K.b[3 + j], x2 = K.b[6 + j];
+    PB[j] = p1 * x2 - p2 * x1;
+    PB[3 + j] = p2 * x0 - p0 * x2;
+    PB[6 + j] = p0 * x1 - p1 * x0;
+    const T y0 = AP[j], y1 = AP[3 + j], y2 = AP[6 + j];
+    PAP[j] = p1 * y2 - p2 * y1;
+    PAP[3 + j] = p2 * y0 - p0 * y2;
+    PAP[6 + j] = p0 * y1 - p1 * y0;
+  }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) K.b[k] -= AP[k];
+  K.c[0] += 2 * PB[0] - PAP[0];
+  K.c[1] += 2 * PB[4] - PAP[4];
+  K.c[2] += 2 * PB[8] - PAP[8];
+  K.c[3] += PB[1] + PB[3] - PAP[1];
+  K.c[4] += PB[2] + PB[6] - PAP[2];
+  K.c[5] += PB[5] + PB[7] - PAP[5];
+}
+
+template <typename T>
+__device__ __forceinline__ void dh_inertia(const LinkDH<T>& C, Sym6<T>& K) {
+  K.a[0] = C.m; K.a[1] = C.m; K.a[2] = C.m; K.a[3] = 0; K.a[4] = 0; K.a[5] = 0;
+  const T h0 = C.h[0], h1 = C.h[1], h2 = C.h[2];
+  K.b[0] = 0;   K.b[1] = h2;  K.b[2] = -h1;
+  K.b[3] = -h2; K.b[4] = 0;   K.b[5] = h0;
+  K.b[6] = h1;  K.b[7] = -h0; K.b[8] = 0;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) K.c[k] = C.I[k];
+}
+
+template <typename T>
+__device__ __forceinline__ void dh_sincos(const LinkDH<T>& C, T q, T* s, T* c) {
+  if (sizeof(T) == 8) {
+    rd_sincos(q + C.th0, s, c);
+  } else {
+    T s0, c0;
+    rd_sincos(q, &s0, &c0);
+    *s = fma(s0, C.cth0, c0 * C.sth0);
+    *c = fma(c0, C.cth0, -(s0 * C.sth0));
+  }
+}
+
+}  // namespace rd

@@ -87,6 +87,10 @@ cudaError_t launch_rnea_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bn
                             int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
                             cudaStream_t st, int* launches);
 template <typename T>
+cudaError_t launch_aba_dh(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd,
+                          int64_t B, const T* q, const T* qd, const T* tau, T* qdd,
+                          T* ws, int64_t ws_slots, cudaStream_t st, int* launches);
+template <typename T>
 cudaError_t launch_fd_scan(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                            int64_t B, const T* q, const T* qd, const T* tau, T* qdd, T* ws,
                            cudaStream_t st, int* launches, bool* supported);
