@@ -58,8 +58,11 @@ typedef enum {
   RD_STRAT_GENERIC = 3,   /* one thread per state, any n, any joints, stash in a global workspace */
   RD_STRAT_REVERSE = 4,   /* one thread per state, any n (all-revolute chains), no stash: the backward
                              sweep re-derives V, Vdot by inverting the forward maps */
-  RD_STRAT_BLOCK_SCAN = 5 /* one CTA per state, thread = link, CTA-wide scans: the single-robot latency
-                             mode for long chains (n <= 512) */
+  RD_STRAT_BLOCK_SCAN = 5, /* one CTA per state, thread = link, CTA-wide scans: the single-robot latency
+                              mode for long chains (n <= 512) */
+  RD_STRAT_WARP_SCAN_EQ13 = 6 /* the paper's operators literally: warp per state, one Eq. (13) semigroup scan
+                                 for V and Vdot (Eq. 12) and the Eq. (16) affine backward scan, body frame;
+                                 n <= 32 */
 } rd_strategy_t;
 
 /* Forward-dynamics algorithm. */

@@ -24,7 +24,8 @@ __all__ = ["Model", "inverse_dynamics", "forward_dynamics", "inverse_dynamics_ho
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librd.so")
 
-STRATEGIES = {"auto": 0, "thread": 1, "warp_scan": 2, "generic": 3, "reverse": 4, "block_scan": 5}
+STRATEGIES = {"auto": 0, "thread": 1, "warp_scan": 2, "generic": 3, "reverse": 4, "block_scan": 5,
+              "warp_scan_eq13": 6}
 _STRAT_NAMES = {v: k for k, v in STRATEGIES.items()}
 FD_ALGOS = {"aba": 0, "jsiia": 1, "aba_scan": 2}
 

@@ -81,7 +81,7 @@ def main():
                 continue
             q, qd, qdd = rnd(n, B, -np.pi, np.pi), rnd(n, B, -1, 1), rnd(n, B, -1, 1)
             out = torch.empty_like(q)
-            for strat in ("thread", "warp_scan", "reverse", "generic", "auto"):
+            for strat in ("thread", "warp_scan", "warp_scan_eq13", "block_scan", "reverse", "generic", "auto"):
                 model.set_strategy(strat)
                 used = model.resolve_strategy(B, dt == torch.float64)
                 if strat != "auto" and used != strat:
