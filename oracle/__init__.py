@@ -183,7 +183,7 @@ def jsi(robot, q):
     return out
 
 
-FD_ALGOS = {"aba": 0, "jsiia": 1, "aba_scan": 2}
+FD_ALGOS = {"aba": 0, "jsiia": 1, "aba_scan": 2, "aba_merged": 3}
 
 
 def fd(robot, q, qd, tau, V0=None, Vd0=None, Ftip=None, g=None, algo="aba",

@@ -678,6 +678,105 @@ std::vector<double> fd_aba_scan(const Chain& c, const double* q, const double* q
   return qdd;
 }
 
+// ABIA with the MERGED backward scan of Eq. (20): one scan of the
+// 15x15 operators acting on x_i = (F_{i-1}, tau_hat_i, zhat_i, chat_{i+1}, 1),
+//   A_i = [[Ad^T_{f_{i-1,i}^{-1}}, 0, 0, 0, Fhat_{i-1}],
+//          [-S_i^T, 0, 0, 0, tau_in_i],
+//          [0, Pi_{i,i+1}, Y_{i,i+1}, 0, 0],
+//          [0, Omega_{i+1}^{-1}, -Omega_{i+1}^{-1} S_{i+1}^T, 0, 0],     (A7: Omega^{-1})
+//          [0, 0, 0, 0, 1]],
+// where F / Fhat are the bias-force recursion of tau_bias (qdd = 0, Eq. 5), so
+// tau_hat_i = tau_in_i - S_i^T F_i.  Seed (A8): (F_n, 0, 0, 0, 1) with
+// F_n = Fhat_n + F_{n+1}; operators for paper index i = n..0 with out-of-range
+// S, Omega^{-1}, Pi, Y, Fhat := 0 (and f_{-1,0} := I).  chat_{i+1} is read from
+// x_i; then the Eq. (19) forward scan gives qdd.
+std::vector<double> fd_aba_merged(const Chain& c, const double* q, const double* qd, const double* tau,
+                                  const V6& V0, const V6& Vd0, const V6& Ftip, int order) {
+  const int n = c.n;
+  std::vector<double> zero(n, 0.0);
+  IdOut bias = rnea(c, q, qd, zero.data(), V0, Vd0, Ftip);      // Fhat of the qdd = 0 recursion
+  std::vector<M4> f = calc_transform(c, q);
+  std::vector<M6> Jh = abi(c, f);
+  std::vector<double> Om(n);
+  std::vector<M6> Y(n);
+  std::vector<V6> Pi(n);
+  for (int i = 0; i < n; ++i) {
+    V6 JS = mv6(Jh[i], c.S[i]);
+    Om[i] = dot6(c.S[i], JS);
+    M6 XT = tr6(Ad(inv4(f[i])));
+    Y[i] = mul6(XT, sub6(eye6(), scale6(outer6(JS, c.S[i]), 1.0 / Om[i])));
+    Pi[i] = scalev(mv6(XT, JS), 1.0 / Om[i]);
+  }
+  const int D = 15;
+  std::function<Dense(const Dense&, const Dense&)> comb =
+      [](const Dense& earlier, const Dense& later) { return dmul(later, earlier, 15); };
+  std::vector<Dense> a;
+  {
+    Dense seed(D * D, 0.0);
+    V6 Fn = addv(bias.Fhat[n - 1], Ftip);
+    for (int r = 0; r < 6; ++r) seed[D * r + 14] = Fn[r];
+    seed[D * 14 + 14] = 1.0;                        // constant map to (F_n, 0, 0, 0, 1)
+    a.push_back(seed);
+  }
+  // paper index i = n..0; 0-based link of paper i is i-1.
+  for (int i = n; i >= 0; --i) {
+    Dense A(D * D, 0.0);
+    const int li = i - 1;                           // link i (0-based), valid if 0 <= li < n
+    const int ln = i;                               // link i+1 (0-based), valid if < n
+    // row block F_{i-1} = Ad^T_{f_{i-1,i}^{-1}} F_i + Fhat_{i-1}
+    if (li >= 0) {
+      M6 L = tr6(Ad(inv4(f[li])));
+      for (int r = 0; r < 6; ++r)
+        for (int s2 = 0; s2 < 6; ++s2) A[D * r + s2] = L[r][s2];
+    } else {
+      for (int r = 0; r < 6; ++r) A[D * r + r] = 1.0;            // f_{-1,0} := I (row unused)
+    }
+    if (li - 1 >= 0) for (int r = 0; r < 6; ++r) A[D * r + 14] = bias.Fhat[li - 1][r];
+    // row tau_hat_i = tau_in_i - S_i^T F_i
+    if (li >= 0) {
+      for (int s2 = 0; s2 < 6; ++s2) A[D * 6 + s2] = -c.S[li][s2];
+      A[D * 6 + 14] = tau[li];
+    }
+    // row block zhat_i = Pi_{i,i+1} tau_hat_{i+1} + Y_{i,i+1} zhat_{i+1}; row chat_{i+1}
+    if (ln < n) {
+      for (int r = 0; r < 6; ++r) {
+        A[D * (7 + r) + 6] = Pi[ln][r];
+        for (int s2 = 0; s2 < 6; ++s2) A[D * (7 + r) + 7 + s2] = Y[ln][r][s2];
+      }
+      A[D * 13 + 6] = 1.0 / Om[ln];
+      for (int s2 = 0; s2 < 6; ++s2) A[D * 13 + 7 + s2] = -c.S[ln][s2] / Om[ln];
+    }
+    A[D * 14 + 14] = 1.0;
+    a.push_back(A);
+  }
+  std::vector<Dense> P = run_scan<Dense>(order, a, comb);
+  std::vector<double> ch(n);
+  for (int i = 0; i <= n - 1; ++i) ch[i] = P[1 + (n - i)][D * 13 + 14];   // x_i holds chat_{i+1} (0-based link i)
+  // Eq. (19) forward scan, as in fd_aba_scan
+  std::function<Dense(const Dense&, const Dense&)> comb8 =
+      [](const Dense& earlier, const Dense& later) { return dmul(later, earlier, 8); };
+  std::vector<Dense> b;
+  {
+    Dense seed(64, 0.0); seed[63] = 1.0;
+    b.push_back(seed);
+  }
+  for (int i = 0; i < n; ++i) {
+    Dense A(64, 0.0);
+    for (int r = 0; r < 6; ++r) {
+      for (int s2 = 0; s2 < 6; ++s2) A[8 * r + s2] = Y[i][s2][r];
+      A[8 * r + 7] = c.S[i][r] * ch[i];
+    }
+    for (int s2 = 0; s2 < 6; ++s2) A[8 * 6 + s2] = -Pi[i][s2];
+    A[8 * 6 + 7] = ch[i];
+    A[63] = 1.0;
+    b.push_back(A);
+  }
+  std::vector<Dense> Q = run_scan<Dense>(order, b, comb8);
+  std::vector<double> qdd(n);
+  for (int i = 0; i < n; ++i) qdd[i] = Q[i + 1][8 * 6 + 7];
+  return qdd;
+}
+
 thread_local std::string g_err;
 
 template <class Fn>
@@ -756,7 +855,8 @@ int orc_jsi(int n, const double* M, const double* S, const double* J, const doub
 }
 
 // Forward dynamics qdd = FD(q, qd, tau, V_0, Vdot_0, F_{n+1}) (Eq. 4).
-// algo: 0 ABIA recursive Eq. (7)-(8); 1 JSIIA Alg. 2; 2 ABIA with Eq. (18)/(19) scans.
+// algo: 0 ABIA recursive Eq. (7)-(8); 1 JSIIA Alg. 2; 2 ABIA with Eq. (18)/(19) scans;
+// 3 ABIA with the merged Eq. (20) backward scan + Eq. (19).
 // Jhat (optional, [n][6][6]) receives the ABI of Eq. (7) for algo 0.
 int orc_fd(int n, const double* M, const double* S, const double* J,
            const double* q, const double* qd, const double* tau,
@@ -771,6 +871,7 @@ int orc_fd(int n, const double* M, const double* S, const double* J,
     if (algo == 0) r = fd_aba(c, q, qd, tau, v0, vd0, ft, &Jh);
     else if (algo == 1) r = fd_jsiia(c, q, qd, tau, v0, vd0, ft);
     else if (algo == 2) r = fd_aba_scan(c, q, qd, tau, v0, vd0, ft, order);
+    else if (algo == 3) r = fd_aba_merged(c, q, qd, tau, v0, vd0, ft, order);
     else throw std::runtime_error("unknown algo");
     std::memcpy(qdd, r.data(), sizeof(double) * n);
     if (Jhat && algo == 0) for (int i = 0; i < n; ++i) store6(Jh[i], Jhat + 36 * i);

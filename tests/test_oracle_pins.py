@@ -395,3 +395,53 @@ def test_batch_equals_single_calls(rng):
         np.testing.assert_array_equal(fb[:, b], oracle.fd(r, q[:, b], qd[:, b], tb[:, b], g=g))
     # empty batch
     assert oracle.rnea_batch(r, g, q[:, :0], qd[:, :0], qdd[:, :0]).shape == (7, 0)
+
+
+@pytest.mark.parametrize("order", ["sequential", "kogge_stone"])
+def test_merged_eq20_scan_equals_aba(order, rng):
+    # Eq. (20) with the Omega^{-1} reading (A7) and the seeding of A8:
+    # the merged 15x15 backward scan reproduces the ABA accelerations.
+    for n in (1, 2, 3, 5, 8, 30):
+        r = synth.random_chain(n, 300 + n, prismatic_fraction=0.3 if n < 30 else 0.0)
+        V0, Vd0, Ft = rng.standard_normal((3, 6))
+        q, qd, tau = rng.uniform(-3, 3, n), rng.uniform(-1, 1, n), rng.standard_normal(n) * 5
+        a = oracle.fd(r, q, qd, tau, V0, Vd0, Ft, algo="aba")
+        m = oracle.fd(r, q, qd, tau, V0, Vd0, Ft, algo="aba_merged", order=order)
+        cond = np.linalg.cond(oracle.jsi(r, q))
+        assert np.abs(m - a).max() <= 1e-14 * max(10.0, cond) * 10 * max(1, np.abs(a).max())
+
+
+def _Q(V):
+    # Q = (w x v, w1^2, w1 w2, w1 w3, w2^2, w2 w3, w3^2)
+    v, w = V[:3], V[3:]
+    return np.concatenate([np.cross(w, v), [w[0] * w[0], w[0] * w[1], w[0] * w[2], w[1] * w[1], w[1] * w[2],
+                                            w[2] * w[2]]])
+
+
+def test_eq15_synchronous_scan_operator_exists_with_block_pattern(rng):
+    # Eq. (15) claims a LINEAR 28-dim recursion on (Vdot, Q, V, Fhat, 1) with the
+    # block pattern of P:233-241 (starred blocks unspecified, A6).  For one link with fixed
+    # (q, qd, qdd), sample previous states (Vdot_{i-1}, V_{i-1}) as the base twist of a 1-link
+    # chain, fit the operator by least squares, and check: exact fit (the map is affine in the
+    # lifted coordinates) and zeros where the paper prints 0.
+    for seed in range(3):
+        r = synth.random_chain(1, 900 + seed, prismatic_fraction=0.5 * seed)
+        q, qd, qdd = rng.uniform(-3, 3, 3)
+        X, Yv = [], []
+        for _ in range(300):
+            V0, Vd0 = rng.standard_normal((2, 6))
+            Fprev = rng.standard_normal(6)
+            _, o = oracle.rnea(r, [q], [qd], [qdd], V0=V0, Vd0=Vd0, full=True)
+            X.append(np.concatenate([Vd0, _Q(V0), V0, Fprev, [1.0]]))
+            Yv.append(np.concatenate([o["Vd"][0], _Q(o["V"][0]), o["V"][0], o["Fhat"][0], [1.0]]))
+        X, Yv = np.array(X), np.array(Yv)
+        A, *_ = np.linalg.lstsq(X, Yv, rcond=None)
+        A = A.T                                               # x_i = A x_{i-1}
+        assert np.abs(X @ A.T - Yv).max() < 1e-9 * np.abs(Yv).max()
+        rows = {"Vdot": slice(0, 6), "Q": slice(6, 15), "V": slice(15, 21), "Fhat": slice(21, 27)}
+        cols = {"Vdot": slice(0, 6), "Q": slice(6, 15), "V": slice(15, 21), "Fhat": slice(21, 27)}
+        zero = [("Vdot", "Q"), ("Vdot", "Fhat"), ("Q", "Vdot"), ("Q", "Fhat"), ("V", "Vdot"), ("V", "Q"),
+                ("V", "Fhat"), ("Fhat", "Fhat")]                   # the 0 entries of P:233-239
+        for rr, cc in zero:
+            assert np.abs(A[rows[rr], cols[cc]]).max() < 1e-8, (rr, cc)
+        np.testing.assert_allclose(A[27], np.eye(28)[27], atol=1e-9)   # last row (0 ... 0 1)
