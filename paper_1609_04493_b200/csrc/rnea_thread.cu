@@ -214,7 +214,7 @@ __device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& 
   g.s = cur[0]; g.c = cur[1];
 }
 
-template <typename T, int W, int UNR>
+template <typename T, int W>
 __global__ void __launch_bounds__(W * 32, 1)
 rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
                       const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
@@ -306,7 +306,6 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
         if (k0 >= k1) return;
         typename TmemIO<T>::Regs r;
         TmemIO<T>::ld(tbase + (uint32_t)((bpar ? k0 : n - 1 - k0) * KC), r);
-#pragma unroll (UNR)
         for (int k = k0; k < k1; ++k) {
           const int slot = bpar ? k : n - 1 - k;
           const int knx = min(k + 1, k1 - 1);
@@ -323,10 +322,8 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
       };
       if (bpar) {
         tmem_seg(0, lt);
-#pragma unroll (UNR)
         for (int k = lt; k < n; ++k) smem_step(k);
       } else {
-#pragma unroll (UNR)
         for (int k = 0; k < n - lt; ++k) smem_step(k);
         tmem_seg(n - lt, n);
       }
@@ -380,23 +377,16 @@ bool thread_kernel_has_n(int n, bool fp64) {
   return fp64 ? plan_for<double>(n, &p) : plan_for<float>(n, &p);
 }
 
-template <typename T, int W, int UNR>
-static cudaError_t launch_wu(const ThreadParams<T>& P, size_t smem, int64_t B, const T* q, const T* qd,
-                             const T* qdd, T* tau, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(rnea_thread_pp_kernel<T, W, UNR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <typename T, int W>
+static cudaError_t launch_w(const ThreadParams<T>& P, size_t smem, int64_t B, const T* q, const T* qd,
+                            const T* qdd, T* tau, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(rnea_thread_pp_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(kSmemCap - 1024));
   if (e != cudaSuccess) return e;
   const int64_t ntiles = (B + W * 32 - 1) / (W * 32);
   const int64_t grid = ntiles < num_sms() ? ntiles : num_sms();
-  rnea_thread_pp_kernel<T, W, UNR><<<(unsigned)grid, W * 32, smem, st>>>(P, B, q, qd, qdd, tau);
+  rnea_thread_pp_kernel<T, W><<<(unsigned)grid, W * 32, smem, st>>>(P, B, q, qd, qdd, tau);
   return cudaGetLastError();
-}
-template <typename T, int W>
-static cudaError_t launch_w(const ThreadParams<T>& P, size_t smem, int64_t B, const T* q, const T* qd,
-                            const T* qdd, T* tau, cudaStream_t st) {
-  static const int unr = getenv("RD_PP_UNROLL") ? atoi(getenv("RD_PP_UNROLL")) : 1;   // A/B knob
-  if (unr == 2) return launch_wu<T, W, 2>(P, smem, B, q, qd, qdd, tau, st);
-  return launch_wu<T, W, 1>(P, smem, B, q, qd, qdd, tau, st);
 }
 
 template <typename T>
