@@ -173,25 +173,43 @@ aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int
 // Ad maps; S = (0, e_z) so U = Jhat[:, 5], D = U[5], u = tau - phat[5].
 template <typename T, int MB>
 __global__ void __launch_bounds__(kAbaThreads, MB)
-aba_dh_kernel(int n, const LinkDH<T>* __restrict__ L, const Boundary<T> bnd, int64_t B,
+aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
               const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ tau_in,
               T* __restrict__ qdd_out, T* __restrict__ ws, int64_t slots) {
+  // model constants staged in shared memory (broadcast reads, no long-scoreboard waits)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LinkDH<T>* L = reinterpret_cast<LinkDH<T>*>(smem_raw);
+  for (int i = threadIdx.x; i < n * (int)(sizeof(LinkDH<T>) / sizeof(T)); i += blockDim.x)
+    reinterpret_cast<T*>(L)[i] = reinterpret_cast<const T*>(Lg)[i];
+  __syncthreads();
   const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= slots) return;
   const T zero6[6] = {0, 0, 0, 0, 0, 0};
   for (int64_t b = slot; b < B; b += slots) {
+    const T* pq = q + b;
+    const T* pqd = qd + b;
+    const T* pt = tau_in + b;
     T V[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) V[k] = bnd.V0[k];
-    for (int i = 0; i < n; ++i) {                 // sweep 1: V_n
-      const LinkDH<T> C = L[i];
-      T s, c;
-      dh_sincos(C, __ldg(q + (int64_t)i * B + b), &s, &c);
-      T Vn[6];
-      dh_ad_finv(C, s, c, V, Vn);
-      Vn[5] += __ldg(qd + (int64_t)i * B + b);
+    // sweep 1: V_n only; inputs two links ahead
+    {
+      T cq = __ldg(pq), cqd = __ldg(pqd);
+      T nq = __ldg(pq + (int64_t)min(1, n - 1) * B), nqd = __ldg(pqd + (int64_t)min(1, n - 1) * B);
+#pragma unroll 2
+      for (int i = 0; i < n; ++i) {
+        const int64_t o = (int64_t)min(i + 2, n - 1) * B;
+        const T fq = __ldg(pq + o), fqd = __ldg(pqd + o);
+        const LinkDH<T>& C = L[i];
+        T s, c;
+        dh_sincos(C, cq, &s, &c);
+        T Vn[6];
+        dh_ad_finv(C, s, c, V, Vn);
+        Vn[5] += cqd;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) V[k] = Vn[k];
+        for (int k = 0; k < 6; ++k) V[k] = Vn[k];
+        cq = nq; cqd = nqd; nq = fq; nqd = fqd;
+      }
     }
     Sym6<T> K, Kc;
     T pc[6];
@@ -199,11 +217,16 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ L, const Boundary<T> bnd, int
     for (int k = 0; k < 6; ++k) { pc[k] = bnd.Ftip[k]; Kc.a[k] = 0; Kc.c[k] = 0; }
 #pragma unroll
     for (int k = 0; k < 9; ++k) Kc.b[k] = 0;
-    for (int i = n - 1; i >= 0; --i) {            // sweep 2
-      const LinkDH<T> C = L[i];
+    // sweep 2 (backward); inputs one link ahead (each iteration is long)
+    T cq = __ldg(pq + (int64_t)(n - 1) * B), cqd = __ldg(pqd + (int64_t)(n - 1) * B),
+      ct = __ldg(pt + (int64_t)(n - 1) * B);
+    for (int i = n - 1; i >= 0; --i) {
+      const int64_t o = (int64_t)max(i - 1, 0) * B;
+      const T nq = __ldg(pq + o), nqd = __ldg(pqd + o), nt = __ldg(pt + o);
+      const LinkDH<T>& C = L[i];
       T s, c;
-      dh_sincos(C, __ldg(q + (int64_t)i * B + b), &s, &c);
-      const T qdi = __ldg(qd + (int64_t)i * B + b);
+      dh_sincos(C, cq, &s, &c);
+      const T qdi = cqd;
       T cc[6] = {qdi * V[1], -qdi * V[0], 0, qdi * V[4], -qdi * V[3], 0};   // ad_V(e_z qd)
       T ph[6];
       bias_force(C, V, zero6, ph);
@@ -216,7 +239,7 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ L, const Boundary<T> bnd, int
       T U[6] = {K.b[2], K.b[5], K.b[8], K.c[4], K.c[5], K.c[2]};
       const T D = U[5];
       const T invD = (D > (T)0) ? (T)1 / D : (T)NAN;
-      const T ub = (__ldg(tau_in + (int64_t)i * B + b) - ph[5]) * invD;
+      const T ub = (ct - ph[5]) * invD;
       T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
 #pragma unroll
       for (int k = 0; k < 6; ++k) w[k * slots] = U[k] * invD;
@@ -236,36 +259,45 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ L, const Boundary<T> bnd, int
         x[5] -= qdi;
         dh_ad_f(C, s, c, x, V);                    // V_{i-1} = Ad_{f_i}(V_i - S qd)
       }
+      cq = nq; cqd = nqd; ct = nt;
     }
+    // sweep 3 (forward): a'_i = X_i a_{i-1} + c_i, qdd_i = ubar_i - Ubar_i . a'_i
     T a[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) { a[k] = bnd.Vd0[k]; V[k] = bnd.V0[k]; }
-    for (int i = 0; i < n; ++i) {                 // sweep 3
-      const LinkDH<T> C = L[i];
-      const T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
-      T Ub[6];
+    {
+      T cq3 = __ldg(pq), cqd3 = __ldg(pqd);
+#pragma unroll 2
+      for (int i = 0; i < n; ++i) {
+        const int64_t o = (int64_t)min(i + 1, n - 1) * B;
+        const T nq3 = __ldg(pq + o), nqd3 = __ldg(pqd + o);
+        const LinkDH<T>& C = L[i];
+        const T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
+        T Ub[6];
 #pragma unroll
-      for (int k = 0; k < 6; ++k) Ub[k] = w[k * slots];
-      const T ub = w[6 * slots];
-      T s, c;
-      dh_sincos(C, __ldg(q + (int64_t)i * B + b), &s, &c);
-      const T qdi = __ldg(qd + (int64_t)i * B + b);
-      T Vn[6], an[6];
-      dh_ad_finv(C, s, c, V, Vn);
-      Vn[5] += qdi;
-      dh_ad_finv(C, s, c, a, an);
-      an[0] = fma(qdi, Vn[1], an[0]);
-      an[1] = fma(-qdi, Vn[0], an[1]);
-      an[3] = fma(qdi, Vn[4], an[3]);
-      an[4] = fma(-qdi, Vn[3], an[4]);
-      T Ua = 0;
+        for (int k = 0; k < 6; ++k) Ub[k] = w[k * slots];
+        const T ub = w[6 * slots];
+        T s, c;
+        dh_sincos(C, cq3, &s, &c);
+        const T qdi = cqd3;
+        T Vn[6], an[6];
+        dh_ad_finv(C, s, c, V, Vn);
+        Vn[5] += qdi;
+        dh_ad_finv(C, s, c, a, an);
+        an[0] = fma(qdi, Vn[1], an[0]);
+        an[1] = fma(-qdi, Vn[0], an[1]);
+        an[3] = fma(qdi, Vn[4], an[3]);
+        an[4] = fma(-qdi, Vn[3], an[4]);
+        T Ua = 0;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) Ua = fma(Ub[k], an[k], Ua);
-      const T qddi = ub - Ua;
-      qdd_out[(int64_t)i * B + b] = qddi;
-      an[5] += qddi;
+        for (int k = 0; k < 6; ++k) Ua = fma(Ub[k], an[k], Ua);
+        const T qddi = ub - Ua;
+        qdd_out[(int64_t)i * B + b] = qddi;
+        an[5] += qddi;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) { a[k] = an[k]; V[k] = Vn[k]; }
+        for (int k = 0; k < 6; ++k) { a[k] = an[k]; V[k] = Vn[k]; }
+        cq3 = nq3; cqd3 = nqd3;
+      }
     }
   }
 }
@@ -275,10 +307,12 @@ cudaError_t launch_aba_dh(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd,
                           const T* qd, const T* tau, T* qdd, T* ws, int64_t ws_slots, cudaStream_t st,
                           int* launches) {
   const int64_t grid = (ws_slots + kAbaThreads - 1) / kAbaThreads;
-  static const int mb = getenv("RD_ABA_MB") ? atoi(getenv("RD_ABA_MB")) : 3;   // A/B knob (occupancy)
-  if (mb == 2) aba_dh_kernel<T, 2><<<(unsigned)grid, kAbaThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots);
-  else if (mb == 4) aba_dh_kernel<T, 4><<<(unsigned)grid, kAbaThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots);
-  else aba_dh_kernel<T, 3><<<(unsigned)grid, kAbaThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots);
+  const size_t smem = (size_t)n * sizeof(LinkDH<T>);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(aba_dh_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  aba_dh_kernel<T, 3><<<(unsigned)grid, kAbaThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots);
   ++*launches;
   return cudaGetLastError();
 }
