@@ -319,14 +319,29 @@ rd_status_t ensure_ws(rd_model_t m, size_t bytes) {
   return RD_OK;
 }
 
+// Device-memory check with a small per-thread cache of recently verified
+// pointers (cudaPointerGetAttributes costs ~1 us per pointer, which dominated the
+// host side of small-batch calls).  Safe under UVA: a device address is never a
+// valid host address, so a cached device pointer cannot later denote host memory.
+thread_local uintptr_t g_ptr_cache[16] = {0};
+thread_local int g_ptr_next = 0;
+
 template <typename T>
 bool is_device_ptr(const T* p) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p);
+  for (uintptr_t c : g_ptr_cache)
+    if (c == a0) return true;
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+  const bool dev = a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+  if (dev) {
+    g_ptr_cache[g_ptr_next] = a0;
+    g_ptr_next = (g_ptr_next + 1) % 16;
+  }
+  return dev;
 }
 
 template <typename T>

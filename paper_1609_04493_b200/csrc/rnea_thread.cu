@@ -380,9 +380,15 @@ bool thread_kernel_has_n(int n, bool fp64) {
 template <typename T, int W>
 static cudaError_t launch_w(const ThreadParams<T>& P, size_t smem, int64_t B, const T* q, const T* qd,
                             const T* qdd, T* tau, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(rnea_thread_pp_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(kSmemCap - 1024));
-  if (e != cudaSuccess) return e;
+  static thread_local int attr_dev = -1;          // the opt-in is per device; set it once
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(rnea_thread_pp_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kSmemCap - 1024));
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
   const int64_t ntiles = (B + W * 32 - 1) / (W * 32);
   const int64_t grid = ntiles < num_sms() ? ntiles : num_sms();
   rnea_thread_pp_kernel<T, W><<<(unsigned)grid, W * 32, smem, st>>>(P, B, q, qd, qdd, tau);

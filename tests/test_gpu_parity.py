@@ -346,3 +346,26 @@ def test_block_scan_long_chains(rd, n):
     q, qd, qdd = synth.states(23, n, 0, 64)
     check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy="block_scan")
     check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, torch.float32, strategy="block_scan")
+
+
+@pytest.mark.parametrize("strategy", ["thread", "warp_scan", "generic", "reverse"])
+def test_cuda_graph_capture_and_replay(rd, strategy):
+    # the launches are stream-ordered and host-synchronisation free, so a batch of
+    # calls can be captured once in a CUDA graph and replayed (launch-bound small batches)
+    cfg = synth.CONFIGS["C2"]
+    q, qd, qdd = synth.states(cfg["seed"], 7, 0, 4000, cfg["ranges"])
+    model = rd.Model.from_robot(synth.arm7(), cfg["gravity"])
+    model.set_strategy(strategy)
+    tq, tqd, tqdd = dev(q), dev(qd), dev(qdd)
+    out = torch.empty_like(tq)
+    ref = rd.inverse_dynamics(model, tq, tqd, tqdd).clone()      # warm-up (allocates any workspace)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        rd.inverse_dynamics(model, tq, tqd, tqdd, out, stream=s)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
