@@ -118,10 +118,15 @@ template <> struct TmemIO<float> {
 // write of the new tile needs.  Every steady-state
 // step is ONE basic block (no branch between the two sweeps), so ptxas can
 // interleave them; the slot kind (TMEM or shared) is fixed per loop segment.
+#ifndef RD_PD
+#define RD_PD 2
+#endif
+constexpr int kPD = RD_PD;   // input prefetch distance (links, stream order over tiles)
+
 template <typename T>
 struct FwdState {
   T V[6], Vd[6];
-  T c_q, c_qd, c_qa, n_q, n_qd, n_qa;   // inputs of the current and the next link (stream order)
+  T a_q[kPD], a_qd[kPD], a_qa[kPD];    // inputs of the next kPD links in stream order ([0] = current)
   const T *pq, *pqd, *pqa;              // this tile's column
   const T *xq, *xqd, *xqa;              // the next tile's column (prefetch across the tile boundary)
 };
@@ -144,12 +149,14 @@ __device__ __forceinline__ void fwd_init(FwdState<T>& f, const ThreadParams<T>& 
   f.pq = q + bl; f.pqd = qd + bl; f.pqa = qdd + bl;
   f.xq = q + bl_next; f.xqd = qd + bl_next; f.xqa = qdd + bl_next;
   if (first) {
-    f.c_q = __ldg(f.pq); f.c_qd = __ldg(f.pqd); f.c_qa = __ldg(f.pqa);
-    const int64_t off1 = (int64_t)(P.n > 1 ? 1 : 0) * B;
-    const T* a = P.n > 1 ? f.pq : f.xq;
-    const T* b = P.n > 1 ? f.pqd : f.xqd;
-    const T* c = P.n > 1 ? f.pqa : f.xqa;
-    f.n_q = __ldg(a + off1); f.n_qd = __ldg(b + off1); f.n_qa = __ldg(c + off1);
+#pragma unroll
+    for (int j = 0; j < kPD; ++j) {
+      const bool here = j < P.n;
+      const int64_t off = (int64_t)(here ? j : min(j - P.n, P.n - 1)) * B;   // n < kPD: reloaded per tile
+      f.a_q[j] = __ldg((here ? f.pq : f.xq) + off);
+      f.a_qd[j] = __ldg((here ? f.pqd : f.xqd) + off);
+      f.a_qa[j] = __ldg((here ? f.pqa : f.xqa) + off);
+    }
   }
 }
 template <typename T>
@@ -165,10 +172,10 @@ __device__ __forceinline__ void fwd_link(FwdState<T>& f, const ThreadParams<T>& 
   // this link's inputs (loaded two links earlier) and the loads for link k+2
   // (stream order over tiles).  (A variant that prefetched into L1 and loaded in
   // place was 20 % slower.)
-  const T cq = f.c_q, cqd = f.c_qd, cqa = f.c_qa;
-  const int k2 = k + 2;
+  const T cq = f.a_q[0], cqd = f.a_qd[0], cqa = f.a_qa[0];
+  const int k2 = k + kPD;
   const bool here = k2 < n;
-  const int64_t off2 = (int64_t)(here ? k2 : min(k2 - n, n - 1)) * B;   // n = 1: reloaded per tile
+  const int64_t off2 = (int64_t)(here ? k2 : min(k2 - n, n - 1)) * B;   // n < kPD: reloaded per tile
   const T f_q = __ldg((here ? f.pq : f.xq) + off2);
   const T f_qd = __ldg((here ? f.pqd : f.xqd) + off2);
   const T f_qa = __ldg((here ? f.pqa : f.xqa) + off2);
@@ -197,8 +204,9 @@ __device__ __forceinline__ void fwd_link(FwdState<T>& f, const ThreadParams<T>& 
   bias_force(C, Vn, Vdn, st + 2);
 #pragma unroll
   for (int j = 0; j < 6; ++j) { f.V[j] = Vn[j]; f.Vd[j] = Vdn[j]; }
-  f.c_q = f.n_q; f.c_qd = f.n_qd; f.c_qa = f.n_qa;
-  f.n_q = f_q; f.n_qd = f_qd; f.n_qa = f_qa;
+#pragma unroll
+  for (int j = 0; j + 1 < kPD; ++j) { f.a_q[j] = f.a_q[j + 1]; f.a_qd[j] = f.a_qd[j + 1]; f.a_qa[j] = f.a_qa[j + 1]; }
+  f.a_q[kPD - 1] = f_q; f.a_qd[kPD - 1] = f_qd; f.a_qa[kPD - 1] = f_qa;
 }
 // backward link i from its stash cur[8]: F_i, tau_i, then (R, p) of link i for link i-1
 template <typename T>
@@ -281,7 +289,7 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
       break;
     }
     const int64_t bn = b + (int64_t)gridDim.x * NT;
-    fwd_init(f, P, B, fvalid ? b : (B - 1), bn < B ? bn : (B - 1), q, qd, qdd, it == 0 || P.n < 2);
+    fwd_init(f, P, B, fvalid ? b : (B - 1), bn < B ? bn : (B - 1), q, qd, qdd, it == 0 || P.n < kPD);
     if (it == 0) {
       // prologue: forward of the first tile alone (parity 0: slot = link)
       for (int k = 0; k < n; ++k) {
