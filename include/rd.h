@@ -70,9 +70,12 @@ typedef enum {
   RD_FD_ABA = 0,          /* articulated-body algorithm, Eq. (7)-(8), Alg. 3 (default) */
   RD_FD_JSIIA = 1,        /* joint-space inertia inversion, Eq. (6)/(17), Alg. 2: n+1 IDs per state
                              (one per lane of a warp) + Cholesky solve; n <= 31, else RD_E_UNSUPPORTED */
-  RD_FD_ABA_SCAN = 2      /* the paper's hybrid ABIA, Alg. 3, all on the GPU: tau_bias by the warp-scan
+  RD_FD_ABA_SCAN = 2,     /* the paper's hybrid ABIA, Alg. 3, all on the GPU: tau_bias by the warp-scan
                              ID, serial ABI (Eq. 7) per state, then the Eq. (18) zhat and Eq. (19)
                              lambda scans across the links of a warp; n <= 32 */
+  RD_FD_ABA_MERGED = 3    /* as RD_FD_ABA_SCAN, but tau_hat, zhat and chat come from ONE backward scan
+                             of the merged Eq. (20) operators (Omega^{-1} reading A7,
+                             seeding A8) over the n+1 lanes of a warp; n <= 31 */
 } rd_fd_algo_t;
 
 /* Library version string. */

@@ -27,7 +27,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librd.so")
 STRATEGIES = {"auto": 0, "thread": 1, "warp_scan": 2, "generic": 3, "reverse": 4, "block_scan": 5,
               "warp_scan_eq13": 6}
 _STRAT_NAMES = {v: k for k, v in STRATEGIES.items()}
-FD_ALGOS = {"aba": 0, "jsiia": 1, "aba_scan": 2}
+FD_ALGOS = {"aba": 0, "jsiia": 1, "aba_scan": 2, "aba_merged": 3}
 
 # Symbols declared in include/rd.h (checked by tests/test_capi.py).
 EXPORTS = [

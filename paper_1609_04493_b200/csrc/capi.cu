@@ -475,13 +475,18 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     return RD_OK;
   }
   std::lock_guard<std::mutex> lk(m->mu);
-  if (m->fd_algo == RD_FD_ABA_SCAN) {
+  if (m->fd_algo == RD_FD_ABA_SCAN || m->fd_algo == RD_FD_ABA_MERGED) {
     st = ensure_ws(m, rd::fd_scan_ws_elems(m->n, batch) * sizeof(T));
     if (st != RD_OK) return st;
     bool ok = false;
-    cudaError_t e = rd::launch_fd_scan<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
-                                          reinterpret_cast<T*>(m->ws), s, &g_launches, &ok);
-    if (!ok) return fail(RD_E_UNSUPPORTED, "scan-ABIA forward dynamics supports n <= 32 (use RD_FD_ABA)");
+    const bool merged = m->fd_algo == RD_FD_ABA_MERGED;
+    cudaError_t e = merged
+        ? rd::launch_fd_merged<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
+                                  reinterpret_cast<T*>(m->ws), s, &g_launches, &ok)
+        : rd::launch_fd_scan<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
+                                reinterpret_cast<T*>(m->ws), s, &g_launches, &ok);
+    if (!ok) return fail(RD_E_UNSUPPORTED, merged ? "merged-scan ABIA forward dynamics supports n <= 31 (use RD_FD_ABA)"
+                                                  : "scan-ABIA forward dynamics supports n <= 32 (use RD_FD_ABA)");
     if (e != cudaSuccess) return cuda_fail(e, "forward dynamics (scan ABIA) launch");
     return RD_OK;
   }
@@ -705,7 +710,7 @@ rd_strategy_t rd_model_resolve_strategy(rd_model_t m, int64_t batch, int32_t fp6
 
 rd_status_t rd_model_set_fd_algo(rd_model_t m, rd_fd_algo_t algo) {
   if (!m) return fail(RD_E_ARG, "null model");
-  if (algo != RD_FD_ABA && algo != RD_FD_JSIIA && algo != RD_FD_ABA_SCAN) return fail(RD_E_ARG, "unknown FD algorithm");
+  if (algo != RD_FD_ABA && algo != RD_FD_JSIIA && algo != RD_FD_ABA_SCAN && algo != RD_FD_ABA_MERGED) return fail(RD_E_ARG, "unknown FD algorithm");
   m->fd_algo = algo;
   return RD_OK;
 }

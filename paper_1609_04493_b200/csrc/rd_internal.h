@@ -69,10 +69,12 @@ template <typename T>
 cudaError_t launch_rnea_generic(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                                 int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
                                 T* ws, int64_t ws_slots, cudaStream_t st, int* launches);
+// qdd == nullptr: qdd = 0; tau == nullptr: not stored; fhat != nullptr: the
+// per-link bias wrench Fhat (joint frame) is stored as [n][6][B].
 template <typename T>
 cudaError_t launch_rnea_warp(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                              int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
-                             cudaStream_t st, int* launches, bool* supported);
+                             cudaStream_t st, int* launches, bool* supported, T* fhat = nullptr);
 template <typename T>
 cudaError_t launch_aba(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                        int64_t B, const T* q, const T* qd, const T* tau, T* qdd,
@@ -98,7 +100,11 @@ template <typename T>
 cudaError_t launch_fd_scan(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                            int64_t B, const T* q, const T* qd, const T* tau, T* qdd, T* ws,
                            cudaStream_t st, int* launches, bool* supported);
-size_t fd_scan_ws_elems(int n, int64_t B);
+template <typename T>
+cudaError_t launch_fd_merged(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
+                             int64_t B, const T* q, const T* qd, const T* tau, T* qdd, T* ws,
+                             cudaStream_t st, int* launches, bool* supported);
+size_t fd_scan_ws_elems(int n, int64_t B);     // workspace (elements) of either scan FD
 template <typename T>
 cudaError_t launch_jsiia(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                          int64_t B, const T* q, const T* qd, const T* tau, T* qdd,

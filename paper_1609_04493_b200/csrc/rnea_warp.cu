@@ -33,7 +33,7 @@ template <typename T>
 __global__ void __launch_bounds__(kWarpCta * 32)
 rnea_warp_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
                  const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
-                 T* __restrict__ tau) {
+                 T* __restrict__ tau, T* __restrict__ fhat) {
   // per-link constants in shared memory, structure-of-arrays [field][32] (lane-contiguous)
   constexpr int NF = sizeof(LinkConst<T>) / sizeof(T);
   __shared__ T sc[NF][32];
@@ -151,6 +151,10 @@ rnea_warp_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> b
     ad_finv(R, p0, p1, p2, V, Vb);
     ad_finv(R, p0, p1, p2, A, Ab);
     bias_force(C, Vb, Ab, Fh);
+    if (fhat && act) {                               // Fhat_l (joint frame) for the merged FD scan, [n][6][B]
+#pragma unroll
+      for (int k = 0; k < 6; ++k) fhat[((int64_t)lane * 6 + k) * B + b] = Fh[k];
+    }
     T F[6];
     const T zero6[6] = {0, 0, 0, 0, 0, 0};
     bwd_step(R, p0, p1, p2, Fh, zero6, F);          // F0hat = Ad^T_{g^-1} Fhat = (R f, p x R f + R m)
@@ -177,29 +181,29 @@ rnea_warp_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> b
     T t = 0;
 #pragma unroll
     for (int k = 0; k < 6; ++k) t = fma(S0[k], F[k], t);
-    if (act) tau[(int64_t)lane * B + b] = t;
+    if (act && tau) tau[(int64_t)lane * B + b] = t;
   }
 }
 
 template <typename T>
 cudaError_t launch_rnea_warp(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                              const T* qd, const T* qdd, T* tau, cudaStream_t st, int* launches,
-                             bool* supported) {
+                             bool* supported, T* fhat) {
   *supported = n >= 1 && n <= 32;
   if (!*supported) return cudaSuccess;
   int64_t grid = (B + kWarpCta - 1) / kWarpCta;
   const int64_t cap = (int64_t)num_sms() * 16;
   if (grid > cap) grid = cap;
-  rnea_warp_kernel<T><<<(unsigned)grid, kWarpCta * 32, 0, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau);
+  rnea_warp_kernel<T><<<(unsigned)grid, kWarpCta * 32, 0, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau, fhat);
   ++*launches;
   return cudaGetLastError();
 }
 
 template cudaError_t launch_rnea_warp<double>(int, const LinkConst<double>*, const Boundary<double>&, int64_t,
                                               const double*, const double*, const double*, double*, cudaStream_t,
-                                              int*, bool*);
+                                              int*, bool*, double*);
 template cudaError_t launch_rnea_warp<float>(int, const LinkConst<float>*, const Boundary<float>&, int64_t,
                                              const float*, const float*, const float*, float*, cudaStream_t, int*,
-                                             bool*);
+                                             bool*, float*);
 
 }  // namespace rd

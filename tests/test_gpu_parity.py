@@ -339,6 +339,48 @@ def test_fd_aba_scan_parity(rd, n, pf):
     assert rd.last_launch_count() == 3
 
 
+# ------------------------------------------------------------------ forward dynamics (merged Eq. 20 scan, NEXT-2)
+@pytest.mark.parametrize("n,pf", [(1, 0.0), (2, 0.0), (7, 0.3), (16, 0.0), (30, 0.0), (31, 0.2)])
+def test_fd_aba_merged_parity(rd, n, pf):
+    r = synth.random_chain(n, 850 + n, prismatic_fraction=pf)
+    g = synth.GRAVITY_Z
+    q, qd, qdd = synth.states(21, n, 0, 1200)
+    tau = oracle.rnea_batch(r, g, q, qd, qdd)
+    model = rd.Model.from_robot(r, g)
+    model.set_fd_algo("aba_merged")
+    out = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()
+    assert np.all(np.isfinite(out))
+    back = oracle.rnea_batch(r, g, q, qd, out)                 # primary: backward error (A14)
+    assert rel_err_per_state(back, tau).max() <= 1e-10
+    sub = np.arange(0, 1200, 37)                                # the oracle's literal Eq. (20) path
+    ref = oracle.fd_batch(r, g, q[:, sub], qd[:, sub], tau[:, sub], algo="aba_merged")
+    assert rel_err_per_state(out[:, sub], ref, floor=1.0).max() < 1e-7
+    assert rd.last_launch_count() == 3
+
+
+@pytest.mark.parametrize("algo", ["aba_scan", "aba_merged"])
+def test_fd_scan_variants_boundary_fp32_limits(rd, algo):
+    n = 9
+    r = synth.random_chain(n, 46, prismatic_fraction=0.2)
+    rng = np.random.default_rng(5)
+    V0, Vd0, Ft = rng.standard_normal((3, 6))
+    model = rd.Model.from_robot(r, (0, 0, 0))
+    model.set_boundary(V0, Vd0, Ft)
+    model.set_fd_algo(algo)
+    q, qd, qdd = synth.states(10, n, 0, 257)
+    tau = np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b], V0, Vd0, Ft) for b in range(257)], 1)
+    out = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()
+    assert rel_err_per_state(out, qdd, floor=1.0).max() < 1e-9
+    out32 = rd.forward_dynamics(model, dev(q, torch.float32), dev(qd, torch.float32),
+                                dev(tau, torch.float32)).cpu().numpy()
+    assert rel_err_per_state(out32, qdd, floor=1.0).max() < 1e-3
+    big = rd.Model.from_robot(synth.random_chain(33, 1), synth.GRAVITY_Z)
+    big.set_fd_algo(algo)
+    z = torch.zeros((33, 10), dtype=torch.float64, device="cuda")
+    with pytest.raises(rd.RdError):
+        rd.forward_dynamics(big, z, z, z)
+
+
 @pytest.mark.parametrize("n", [33, 100, 257, 512])
 def test_block_scan_long_chains(rd, n):
     # NEXT-3 single-robot latency mode: one CTA per state, CTA-wide scans

@@ -23,8 +23,8 @@ for dt in (torch.float64, torch.float32):
                 model.set_strategy(strat)
                 rd.inverse_dynamics(model, q, qd, qdd)
             tau = rd.inverse_dynamics(model, q, qd, qdd)
-            for algo in ("aba", "jsiia", "aba_scan"):
-                if (algo == "jsiia" and n > 31) or (algo == "aba_scan" and n > 32):
+            for algo in ("aba", "jsiia", "aba_scan", "aba_merged"):
+                if (algo in ("jsiia", "aba_merged") and n > 31) or (algo == "aba_scan" and n > 32):
                     continue
                 model.set_fd_algo(algo)
                 rd.forward_dynamics(model, q, qd, tau)

@@ -102,8 +102,8 @@ def main():
             model.set_fd_algo("aba")
             tau = rd.inverse_dynamics(model, q, qd, qdd)
             out = torch.empty_like(q)
-            for algo in ("aba", "jsiia", "aba_scan"):
-                if (algo == "jsiia" and n > 31) or (algo == "aba_scan" and n > 32):
+            for algo in ("aba", "jsiia", "aba_scan", "aba_merged"):
+                if (algo in ("jsiia", "aba_merged") and n > 31) or (algo == "aba_scan" and n > 32):
                     continue
                 model.set_fd_algo(algo)
                 ms = time_call(lambda: rd.forward_dynamics(model, q, qd, tau, out), 10)
