@@ -134,6 +134,19 @@ rd_status_t rd_forward_dynamics_f32(rd_model_t m, int64_t batch, const float* q,
                                     const float* tau, float* qdd, void* stream);
 rd_status_t rd_model_set_fd_algo(rd_model_t m, rd_fd_algo_t algo);
 
+/* Forward dynamics with a per-state status array (NEXT-4, SURVEY §8(b) "Errors";
+ * A11).  As rd_forward_dynamics_*, plus status: DEVICE int32[batch] (NULL =
+ * none, same as the plain call), written for every state: 0 = all pivots
+ * positive; k > 0 = the algorithm's pivot at 1-based link k was not positive
+ * (ABA / ABA_SCAN / ABA_MERGED: the tip-most link with Omega_k = S_k^T Jhat_k S_k
+ * <= 0 in the ABI sweep, Eq. 7; JSIIA: the first non-positive Cholesky pivot of
+ * M(q)).  A failing state's qdd is NaN and other states are unaffected.
+ * status must be 4-byte aligned device memory not overlapping qdd (RD_E_ARG). */
+rd_status_t rd_forward_dynamics_ex_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                       const double* tau, double* qdd, int32_t* status, void* stream);
+rd_status_t rd_forward_dynamics_ex_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,
+                                       const float* tau, float* qdd, int32_t* status, void* stream);
+
 /* End-to-end inverse dynamics on HOST arrays [n][batch] (pageable or pinned):
  * the library streams the batch through device buffers in chunks, overlapping
  * host->device copies, the kernel and device->host copies on its own streams,

@@ -35,7 +35,7 @@ EXPORTS = [
     "rd_model_set_strategy", "rd_model_resolve_strategy", "rd_model_set_boundary",
     "rd_inverse_dynamics_f64", "rd_inverse_dynamics_f32", "rd_forward_dynamics_f64",
     "rd_forward_dynamics_f32", "rd_model_set_fd_algo", "rd_inverse_dynamics_host_f64",
-    "rd_last_launch_count",
+    "rd_last_launch_count", "rd_forward_dynamics_ex_f64", "rd_forward_dynamics_ex_f32",
 ]
 
 
@@ -69,6 +69,8 @@ def lib():
         for name in ("rd_inverse_dynamics_f64", "rd_inverse_dynamics_f32",
                      "rd_forward_dynamics_f64", "rd_forward_dynamics_f32"):
             getattr(L, name).argtypes = [vp, i64, vp, vp, vp, vp, vp]
+        for name in ("rd_forward_dynamics_ex_f64", "rd_forward_dynamics_ex_f32"):
+            getattr(L, name).argtypes = [vp, i64, vp, vp, vp, vp, vp, vp]
         L.rd_inverse_dynamics_host_f64.argtypes = [vp, i64, vp, vp, vp, vp]
         L.rd_last_launch_count.restype = i32
         for name in EXPORTS:
@@ -180,16 +182,27 @@ def inverse_dynamics(model: Model, q, qd, qdd, out=None, stream=None):
     return out
 
 
-def forward_dynamics(model: Model, q, qd, tau, out=None, stream=None):
-    """qdd = FD(q, qd, tau) (Eq. 4, ABA Eq. 7-8) for B states; torch CUDA tensors [n, B]."""
+def forward_dynamics(model: Model, q, qd, tau, out=None, stream=None, status=None):
+    """qdd = FD(q, qd, tau) (Eq. 4, ABA Eq. 7-8) for B states; torch CUDA tensors [n, B].
+
+    status: optional int32 CUDA tensor [B] (rd_forward_dynamics_ex_*): 0, or the
+    1-based link of the failing pivot of that state (its qdd is NaN)."""
     import torch
     dt = _check_tensors(model, q, qd, tau)
     if out is None:
         out = torch.empty_like(q)
     _check_tensors(model, q, out)
-    f = lib().rd_forward_dynamics_f64 if dt == torch.float64 else lib().rd_forward_dynamics_f32
+    if status is None:
+        f = lib().rd_forward_dynamics_f64 if dt == torch.float64 else lib().rd_forward_dynamics_f32
+        _check(f(model.handle, q.shape[1], q.data_ptr(), qd.data_ptr(), tau.data_ptr(), out.data_ptr(),
+                 _stream_ptr(stream)), "rd_forward_dynamics")
+        return out
+    if status.dtype != torch.int32 or status.device != q.device or status.shape != (q.shape[1],) \
+            or not status.is_contiguous():
+        raise RdError("status must be a contiguous int32 [B] tensor on the inputs' device")
+    f = lib().rd_forward_dynamics_ex_f64 if dt == torch.float64 else lib().rd_forward_dynamics_ex_f32
     _check(f(model.handle, q.shape[1], q.data_ptr(), qd.data_ptr(), tau.data_ptr(), out.data_ptr(),
-             _stream_ptr(stream)), "rd_forward_dynamics")
+             status.data_ptr(), _stream_ptr(stream)), "rd_forward_dynamics_ex")
     return out
 
 

@@ -36,7 +36,7 @@ template <typename T>
 __global__ void __launch_bounds__(kAbaThreads)
 aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int64_t B,
            const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ tau_in,
-           T* __restrict__ qdd_out, T* __restrict__ ws, int64_t slots) {
+           T* __restrict__ qdd_out, T* __restrict__ ws, int64_t slots, int32_t* __restrict__ status) {
   const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= slots) return;
   const T zero6[6] = {0, 0, 0, 0, 0, 0};
@@ -62,6 +62,7 @@ aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int
     //      V_{i-1} = Ad_{f_i}(V_i - S_i qd_i); stores Ubar = U/D and ubar = u/D (7 per link)
     Sym6<T> K, Kc;
     T ph[6], pc[6];
+    int fail = 0;                                         // tip-most link with Omega <= 0 (1-based)
 #pragma unroll
     for (int k = 0; k < 6; ++k) pc[k] = bnd.Ftip[k];   // F_{n+1} enters link n like a bias wrench
 #pragma unroll
@@ -99,6 +100,7 @@ aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int
       const T D = fma(C.beta, U[2], C.alpha * U[5]);
       const T u = __ldg(tau_in + (int64_t)i * B + b) - fma(C.beta, ph[2], C.alpha * ph[5]);
       const T invD = (D > (T)0) ? (T)1 / D : (T)NAN;      // A11: per-state NaN
+      if (!(D > (T)0) && fail == 0) fail = i + 1;
       const T ub = u * invD;
       T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
 #pragma unroll
@@ -128,6 +130,7 @@ aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int
         V[3] = wr[0]; V[4] = wr[1]; V[5] = wr[2];
       }
     }
+    if (status) status[b] = fail;
     // ---- sweep 3 (forward, the role of Eq. 19): V_i and c_i again, a'_i = X_i a_{i-1} + c_i,
     //      qdd_i = ubar_i - Ubar_i . a'_i, a_i = a'_i + S_i qdd_i
     T a[6];
@@ -175,7 +178,7 @@ template <typename T, int MB>
 __global__ void __launch_bounds__(kAbaThreads, MB)
 aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
               const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ tau_in,
-              T* __restrict__ qdd_out, T* __restrict__ ws, int64_t slots) {
+              T* __restrict__ qdd_out, T* __restrict__ ws, int64_t slots, int32_t* __restrict__ status) {
   // model constants staged in shared memory (broadcast reads, no long-scoreboard waits)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LinkDH<T>* L = reinterpret_cast<LinkDH<T>*>(smem_raw);
@@ -213,6 +216,7 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
     }
     Sym6<T> K, Kc;
     T pc[6];
+    int fail = 0;                                         // tip-most link with Omega <= 0 (1-based)
 #pragma unroll
     for (int k = 0; k < 6; ++k) { pc[k] = bnd.Ftip[k]; Kc.a[k] = 0; Kc.c[k] = 0; }
 #pragma unroll
@@ -239,6 +243,7 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
       T U[6] = {K.b[2], K.b[5], K.b[8], K.c[4], K.c[5], K.c[2]};
       const T D = U[5];
       const T invD = (D > (T)0) ? (T)1 / D : (T)NAN;
+      if (!(D > (T)0) && fail == 0) fail = i + 1;
       const T ub = (ct - ph[5]) * invD;
       T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
 #pragma unroll
@@ -261,6 +266,7 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
       }
       cq = nq; cqd = nqd; ct = nt;
     }
+    if (status) status[b] = fail;
     // sweep 3 (forward): a'_i = X_i a_{i-1} + c_i, qdd_i = ubar_i - Ubar_i . a'_i
     T a[6];
 #pragma unroll
@@ -305,39 +311,39 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
 template <typename T>
 cudaError_t launch_aba_dh(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                           const T* qd, const T* tau, T* qdd, T* ws, int64_t ws_slots, cudaStream_t st,
-                          int* launches) {
+                          int* launches, int32_t* status) {
   const int64_t grid = (ws_slots + kAbaThreads - 1) / kAbaThreads;
   const size_t smem = (size_t)n * sizeof(LinkDH<T>);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(aba_dh_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  aba_dh_kernel<T, 3><<<(unsigned)grid, kAbaThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots);
+  aba_dh_kernel<T, 3><<<(unsigned)grid, kAbaThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots, status);
   ++*launches;
   return cudaGetLastError();
 }
 template cudaError_t launch_aba_dh<double>(int, const LinkDH<double>*, const Boundary<double>&, int64_t,
                                            const double*, const double*, const double*, double*, double*, int64_t,
-                                           cudaStream_t, int*);
+                                           cudaStream_t, int*, int32_t*);
 template cudaError_t launch_aba_dh<float>(int, const LinkDH<float>*, const Boundary<float>&, int64_t,
                                           const float*, const float*, const float*, float*, float*, int64_t,
-                                          cudaStream_t, int*);
+                                          cudaStream_t, int*, int32_t*);
 
 template <typename T>
 cudaError_t launch_aba(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                        const T* qd, const T* tau, T* qdd, T* ws, int64_t ws_slots, cudaStream_t st,
-                       int* launches) {
+                       int* launches, int32_t* status) {
   const int64_t grid = (ws_slots + kAbaThreads - 1) / kAbaThreads;
-  aba_kernel<T><<<(unsigned)grid, kAbaThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots);
+  aba_kernel<T><<<(unsigned)grid, kAbaThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots, status);
   ++*launches;
   return cudaGetLastError();
 }
 
 template cudaError_t launch_aba<double>(int, const LinkConst<double>*, const Boundary<double>&, int64_t,
                                         const double*, const double*, const double*, double*, double*, int64_t,
-                                        cudaStream_t, int*);
+                                        cudaStream_t, int*, int32_t*);
 template cudaError_t launch_aba<float>(int, const LinkConst<float>*, const Boundary<float>&, int64_t,
                                        const float*, const float*, const float*, float*, float*, int64_t,
-                                       cudaStream_t, int*);
+                                       cudaStream_t, int*, int32_t*);
 
 }  // namespace rd

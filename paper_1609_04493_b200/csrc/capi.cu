@@ -461,15 +461,23 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
 
 template <typename T>
 rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* qd, const T* tau, T* qdd,
-                             void* stream) {
+                             void* stream, int32_t* status = nullptr) {
   g_launches = 0;
   rd_status_t st = check_io<T>(m, batch, q, qd, tau, qdd, true);
   if (st != RD_OK || batch == 0) return st;
+  if (status) {
+    if (reinterpret_cast<uintptr_t>(status) % sizeof(int32_t) != 0) return fail(RD_E_ARG, "misaligned pointer: status");
+    if (!is_device_ptr(status)) return fail(RD_E_ARG, "not device memory: status");
+    const char* so = reinterpret_cast<const char*>(status);
+    const char* qo = reinterpret_cast<const char*>(qdd);
+    const size_t sb = (size_t)batch * sizeof(int32_t), qb = (size_t)m->n * (size_t)batch * sizeof(T);
+    if (so < qo + qb && qo < so + sb) return fail(RD_E_ARG, "status aliases qdd");
+  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (m->fd_algo == RD_FD_JSIIA) {
     bool ok = false;
     cudaError_t e = rd::launch_jsiia<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd, s,
-                                        &g_launches, &ok);
+                                        &g_launches, &ok, status);
     if (!ok) return fail(RD_E_UNSUPPORTED, "JSIIA forward dynamics supports n <= 31 (use RD_FD_ABA)");
     if (e != cudaSuccess) return cuda_fail(e, "forward dynamics (JSIIA) launch");
     return RD_OK;
@@ -482,9 +490,9 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     const bool merged = m->fd_algo == RD_FD_ABA_MERGED;
     cudaError_t e = merged
         ? rd::launch_fd_merged<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
-                                  reinterpret_cast<T*>(m->ws), s, &g_launches, &ok)
+                                  reinterpret_cast<T*>(m->ws), s, &g_launches, &ok, status)
         : rd::launch_fd_scan<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
-                                reinterpret_cast<T*>(m->ws), s, &g_launches, &ok);
+                                reinterpret_cast<T*>(m->ws), s, &g_launches, &ok, status);
     if (!ok) return fail(RD_E_UNSUPPORTED, merged ? "merged-scan ABIA forward dynamics supports n <= 31 (use RD_FD_ABA)"
                                                   : "scan-ABIA forward dynamics supports n <= 32 (use RD_FD_ABA)");
     if (e != cudaSuccess) return cuda_fail(e, "forward dynamics (scan ABIA) launch");
@@ -496,9 +504,9 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   static const bool no_dh = getenv("RD_ABA_NODH") && getenv("RD_ABA_NODH")[0] == '1';   // A/B knob
   cudaError_t e = (m->dh_ok && !no_dh)
       ? rd::launch_aba_dh<T>(m->n, dh_dev<T>(m), dh_bnd<T>(m), batch, q, qd, tau, qdd,
-                             reinterpret_cast<T*>(m->ws), slots, s, &g_launches)
+                             reinterpret_cast<T*>(m->ws), slots, s, &g_launches, status)
       : rd::launch_aba<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
-                          reinterpret_cast<T*>(m->ws), slots, s, &g_launches);
+                          reinterpret_cast<T*>(m->ws), slots, s, &g_launches, status);
   if (e != cudaSuccess) return cuda_fail(e, "forward dynamics launch");
   return RD_OK;
 }
@@ -744,6 +752,14 @@ rd_status_t rd_forward_dynamics_f64(rd_model_t m, int64_t batch, const double* q
 rd_status_t rd_forward_dynamics_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,
                                     const float* tau, float* qdd, void* stream) {
   return forward_dynamics<float>(m, batch, q, qd, tau, qdd, stream);
+}
+rd_status_t rd_forward_dynamics_ex_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                       const double* tau, double* qdd, int32_t* status, void* stream) {
+  return forward_dynamics<double>(m, batch, q, qd, tau, qdd, stream, status);
+}
+rd_status_t rd_forward_dynamics_ex_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,
+                                       const float* tau, float* qdd, int32_t* status, void* stream) {
+  return forward_dynamics<float>(m, batch, q, qd, tau, qdd, stream, status);
 }
 
 // Host-buffer pipeline: chunks of `hchunk` states; chunk k uses device buffer

@@ -35,13 +35,15 @@ constexpr int kPiPerLink = 7;          // Pi (6), Omega (1)
 // ---------------------------------------------------------------- Alg. 3 lines 3-4
 template <typename T>
 __global__ void __launch_bounds__(kAbiThreads)
-abi_kernel(int n, const LinkConst<T>* __restrict__ L, int64_t B, const T* __restrict__ q, T* __restrict__ pi_ws) {
+abi_kernel(int n, const LinkConst<T>* __restrict__ L, int64_t B, const T* __restrict__ q, T* __restrict__ pi_ws,
+           int32_t* __restrict__ status) {
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
     Sym6<T> K, Kc;
 #pragma unroll
     for (int k = 0; k < 6; ++k) { Kc.a[k] = 0; Kc.c[k] = 0; }
 #pragma unroll
     for (int k = 0; k < 9; ++k) Kc.b[k] = 0;
+    int fail = 0;                                   // tip-most link with Omega <= 0 (1-based)
     for (int j = n - 1; j >= 0; --j) {
       const LinkConst<T> C = L[j];
       Rot<T> R;
@@ -60,6 +62,7 @@ abi_kernel(int n, const LinkConst<T>* __restrict__ L, int64_t B, const T* __rest
       }
       const T D = fma(C.beta, U[2], C.alpha * U[5]);
       const T invD = (D > (T)0) ? (T)1 / D : (T)NAN;
+      if (!(D > (T)0) && fail == 0) fail = j + 1;
       // Pi_j = X_j^T U / D = (R u_f, p x R u_f + R u_m) / D
       T Ud[6], Pi[6];
 #pragma unroll
@@ -75,6 +78,7 @@ abi_kernel(int n, const LinkConst<T>* __restrict__ L, int64_t B, const T* __rest
         congruence(R, p0, p1, p2, K, Kc);
       }
     }
+    if (status) status[b] = fail;
   }
 }
 
@@ -420,7 +424,7 @@ fd_merged_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> b
 template <typename T>
 cudaError_t launch_fd_scan(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                            const T* qd, const T* tau, T* qdd, T* ws, cudaStream_t st, int* launches,
-                           bool* supported) {
+                           bool* supported, int32_t* status) {
   *supported = n >= 1 && n <= 32;
   if (!*supported) return cudaSuccess;
   T* tau_bias = ws;                                  // [n][B]
@@ -430,7 +434,7 @@ cudaError_t launch_fd_scan(int n, const LinkConst<T>* L_dev, const Boundary<T>& 
   if (e != cudaSuccess) return e;
   int64_t g1 = (B + kAbiThreads - 1) / kAbiThreads;
   if (g1 > (int64_t)num_sms() * 8) g1 = (int64_t)num_sms() * 8;
-  abi_kernel<T><<<(unsigned)g1, kAbiThreads, 0, st>>>(n, L_dev, B, q, pi_ws);                          // lines 3-4
+  abi_kernel<T><<<(unsigned)g1, kAbiThreads, 0, st>>>(n, L_dev, B, q, pi_ws, status);                          // lines 3-4
   ++*launches;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -444,7 +448,7 @@ cudaError_t launch_fd_scan(int n, const LinkConst<T>* L_dev, const Boundary<T>& 
 template <typename T>
 cudaError_t launch_fd_merged(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                              const T* qd, const T* tau, T* qdd, T* ws, cudaStream_t st, int* launches,
-                             bool* supported) {
+                             bool* supported, int32_t* status) {
   *supported = n >= 1 && n <= 31;                   // n + 1 operators on the lanes of one warp
   if (!*supported) return cudaSuccess;
   T* fhat_ws = ws;                                   // [n][6][B]
@@ -454,7 +458,7 @@ cudaError_t launch_fd_merged(int n, const LinkConst<T>* L_dev, const Boundary<T>
   if (e != cudaSuccess) return e;
   int64_t g1 = (B + kAbiThreads - 1) / kAbiThreads;
   if (g1 > (int64_t)num_sms() * 8) g1 = (int64_t)num_sms() * 8;
-  abi_kernel<T><<<(unsigned)g1, kAbiThreads, 0, st>>>(n, L_dev, B, q, pi_ws);
+  abi_kernel<T><<<(unsigned)g1, kAbiThreads, 0, st>>>(n, L_dev, B, q, pi_ws, status);
   ++*launches;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -478,15 +482,15 @@ size_t fd_scan_ws_elems(int n, int64_t B) { return (size_t)n * B * (6 + kPiPerLi
 
 template cudaError_t launch_fd_scan<double>(int, const LinkConst<double>*, const Boundary<double>&, int64_t,
                                             const double*, const double*, const double*, double*, double*,
-                                            cudaStream_t, int*, bool*);
+                                            cudaStream_t, int*, bool*, int32_t*);
 template cudaError_t launch_fd_merged<double>(int, const LinkConst<double>*, const Boundary<double>&, int64_t,
                                               const double*, const double*, const double*, double*, double*,
-                                              cudaStream_t, int*, bool*);
+                                              cudaStream_t, int*, bool*, int32_t*);
 template cudaError_t launch_fd_merged<float>(int, const LinkConst<float>*, const Boundary<float>&, int64_t,
                                              const float*, const float*, const float*, float*, float*,
-                                             cudaStream_t, int*, bool*);
+                                             cudaStream_t, int*, bool*, int32_t*);
 template cudaError_t launch_fd_scan<float>(int, const LinkConst<float>*, const Boundary<float>&, int64_t,
                                            const float*, const float*, const float*, float*, float*, cudaStream_t,
-                                           int*, bool*);
+                                           int*, bool*, int32_t*);
 
 }  // namespace rd

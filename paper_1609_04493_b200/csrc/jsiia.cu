@@ -41,7 +41,7 @@ template <typename T>
 __global__ void __launch_bounds__(kJsWarps * 32)
 jsiia_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
              const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ tau_in,
-             T* __restrict__ qdd_out) {
+             T* __restrict__ qdd_out, int32_t* __restrict__ status) {
   constexpr int NF = sizeof(LinkConst<T>) / sizeof(T);
   __shared__ T sc[NF][32];                  // link constants [field][link]
   __shared__ T strf[kJsWarps][3][32];       // per-state link transforms (sin, cos, d)
@@ -142,8 +142,10 @@ jsiia_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> bnd, 
     // ---- tau_diff = tau - tau_bias; Cholesky M = L L^T; solve (Alg. 2 lines 2-4)
     T rhs = (lane < n) ? taul - M[lane][31] : T(0);
     bool spd = true;
+    int fail = 0;                                   // first non-positive Cholesky pivot (1-based)
     for (int k = 0; k < n; ++k) {
       const T piv = M[k][k];
+      if (spd && !(piv > T(0))) fail = k + 1;
       spd = spd && (piv > T(0));
       const T lkk = sqrt(piv > T(0) ? piv : T(1));
       __syncwarp();
@@ -168,28 +170,30 @@ jsiia_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> bnd, 
       if (lane < i) rhs = fma(-M[i][lane], xi, rhs);
     }
     if (lane < n) qdd_out[(int64_t)lane * B + b] = spd ? rhs : T(NAN);
+    if (status && lane == 0) status[b] = fail;
     __syncwarp();
   }
 }
 
 template <typename T>
 cudaError_t launch_jsiia(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
-                         const T* qd, const T* tau, T* qdd, cudaStream_t st, int* launches, bool* supported) {
+                         const T* qd, const T* tau, T* qdd, cudaStream_t st, int* launches, bool* supported,
+                         int32_t* status) {
   *supported = n >= 1 && n <= 31;
   if (!*supported) return cudaSuccess;
   int64_t grid = (B + kJsWarps - 1) / kJsWarps;
   const int64_t cap = (int64_t)num_sms() * 16;
   if (grid > cap) grid = cap;
-  jsiia_kernel<T><<<(unsigned)grid, kJsWarps * 32, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd);
+  jsiia_kernel<T><<<(unsigned)grid, kJsWarps * 32, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, status);
   ++*launches;
   return cudaGetLastError();
 }
 
 template cudaError_t launch_jsiia<double>(int, const LinkConst<double>*, const Boundary<double>&, int64_t,
                                           const double*, const double*, const double*, double*, cudaStream_t,
-                                          int*, bool*);
+                                          int*, bool*, int32_t*);
 template cudaError_t launch_jsiia<float>(int, const LinkConst<float>*, const Boundary<float>&, int64_t,
                                          const float*, const float*, const float*, float*, cudaStream_t, int*,
-                                         bool*);
+                                         bool*, int32_t*);
 
 }  // namespace rd

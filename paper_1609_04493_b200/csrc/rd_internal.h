@@ -60,7 +60,10 @@ enum Strategy { kAuto = 0, kThread = 1, kWarpScan = 2, kGeneric = 3 };
 
 // Launchers (rnea_thread.cu / rnea_generic.cu / rnea_warp.cu / aba.cu).
 // All return cudaGetLastError() after enqueue.  `launches` is incremented by
-// the number of kernels enqueued.
+// the number of kernels enqueued.  FD launchers take an optional per-state
+// status array (device int32[B], nullptr = none): 0, or the 1-based link of the
+// failing pivot (Omega_i <= 0 in the ABI sweep, tip-most first; JSIIA: the first
+// non-positive Cholesky pivot).
 template <typename T>
 cudaError_t launch_rnea_thread(int n, const LinkDH<T>* L_host, const Boundary<T>& bnd,
                                int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
@@ -78,7 +81,7 @@ cudaError_t launch_rnea_warp(int n, const LinkConst<T>* L_dev, const Boundary<T>
 template <typename T>
 cudaError_t launch_aba(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                        int64_t B, const T* q, const T* qd, const T* tau, T* qdd,
-                       T* ws, int64_t ws_slots, cudaStream_t st, int* launches);
+                       T* ws, int64_t ws_slots, cudaStream_t st, int* launches, int32_t* status);
 
 template <typename T>
 cudaError_t launch_rnea_warp13(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
@@ -95,20 +98,20 @@ cudaError_t launch_rnea_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bn
 template <typename T>
 cudaError_t launch_aba_dh(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd,
                           int64_t B, const T* q, const T* qd, const T* tau, T* qdd,
-                          T* ws, int64_t ws_slots, cudaStream_t st, int* launches);
+                          T* ws, int64_t ws_slots, cudaStream_t st, int* launches, int32_t* status);
 template <typename T>
 cudaError_t launch_fd_scan(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                            int64_t B, const T* q, const T* qd, const T* tau, T* qdd, T* ws,
-                           cudaStream_t st, int* launches, bool* supported);
+                           cudaStream_t st, int* launches, bool* supported, int32_t* status);
 template <typename T>
 cudaError_t launch_fd_merged(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                              int64_t B, const T* q, const T* qd, const T* tau, T* qdd, T* ws,
-                             cudaStream_t st, int* launches, bool* supported);
+                             cudaStream_t st, int* launches, bool* supported, int32_t* status);
 size_t fd_scan_ws_elems(int n, int64_t B);     // workspace (elements) of either scan FD
 template <typename T>
 cudaError_t launch_jsiia(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                          int64_t B, const T* q, const T* qd, const T* tau, T* qdd,
-                         cudaStream_t st, int* launches, bool* supported);
+                         cudaStream_t st, int* launches, bool* supported, int32_t* status);
 
 // Workspace slots (threads) the generic / ABA kernels use: ws holds
 // per-link doubles for each slot (see the .cu files for the layout).

@@ -381,6 +381,40 @@ def test_fd_scan_variants_boundary_fp32_limits(rd, algo):
         rd.forward_dynamics(big, z, z, z)
 
 
+@pytest.mark.parametrize("algo", ["aba", "jsiia", "aba_scan", "aba_merged"])
+@pytest.mark.parametrize("dh", [True, False])
+def test_fd_status_array(rd, algo, dh):
+    # NEXT-4: per-state status (rd_forward_dynamics_ex_*).  A NaN joint angle at
+    # 0-based link j >= 1 makes the articulated inertia of link j-1 NaN, so the
+    # ABI pivot Omega fails first at 1-based link j; JSIIA's first Cholesky pivot
+    # M_11 depends on every q_j (j >= 1).  Other states are unaffected.
+    n = 8
+    r = synth.random_chain(n, 47, prismatic_fraction=0.0 if dh else 0.3)
+    g = synth.GRAVITY_Z
+    q, qd, qdd = synth.states(11, n, 0, 96)
+    tau = oracle.rnea_batch(r, g, q, qd, qdd)
+    bad = {5: 3, 9: 1, 40: 7}
+    for b, j in bad.items():
+        q[j, b] = np.nan
+    model = rd.Model.from_robot(r, g)
+    model.set_fd_algo(algo)
+    st = torch.full((96,), -7, dtype=torch.int32, device="cuda")
+    out = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau), status=st).cpu().numpy()
+    st = st.cpu().numpy()
+    good = np.setdiff1d(np.arange(96), list(bad))
+    assert np.all(st[good] == 0)
+    assert rel_err_per_state(out[:, good], qdd[:, good], floor=1.0).max() < 1e-9
+    for b, j in bad.items():
+        assert st[b] == (1 if algo == "jsiia" else j), (b, st[b])
+        assert not np.all(np.isfinite(out[:, b]))
+    out2 = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()   # plain call, same qdd
+    np.testing.assert_array_equal(np.isfinite(out2), np.isfinite(out))
+    np.testing.assert_array_equal(out2[:, good], out[:, good])
+    with pytest.raises(rd.RdError):
+        rd.forward_dynamics(model, dev(q), dev(qd), dev(tau), status=torch.zeros(95, dtype=torch.int32,
+                                                                                   device="cuda"))
+
+
 @pytest.mark.parametrize("n", [33, 100, 257, 512])
 def test_block_scan_long_chains(rd, n):
     # NEXT-3 single-robot latency mode: one CTA per state, CTA-wide scans
