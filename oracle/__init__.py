@@ -53,10 +53,11 @@ def lib():
             getattr(L, name).restype = None
         L.orc_rnea.argtypes = [i32, d, d, d, d, d, d, d, d, d, i32, i32, d, d, d, d, d]
         L.orc_jsi.argtypes = [i32, d, d, d, d, d]
+        L.orc_eq15_operator.argtypes = [d, d, d, ctypes.c_double, ctypes.c_double, ctypes.c_double, d]
         L.orc_fd.argtypes = [i32, d, d, d, d, d, d, d, d, d, i32, i32, d, d]
         L.orc_rnea_batch.argtypes = [i32, d, d, d, d, i64, d, d, d, d, i32]
         L.orc_fd_batch.argtypes = [i32, d, d, d, d, i64, d, d, d, d, i32, i32]
-        for name in ("orc_rnea", "orc_jsi", "orc_fd", "orc_rnea_batch", "orc_fd_batch"):
+        for name in ("orc_rnea", "orc_jsi", "orc_fd", "orc_rnea_batch", "orc_fd_batch", "orc_eq15_operator"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -148,7 +149,7 @@ def velacc_lift13(a):
 
 
 # ------------------------------------------------------------------ dynamics
-RNEA_VARIANTS = {"recursive": 0, "split": 1, "fused": 2, "lift": 3}
+RNEA_VARIANTS = {"recursive": 0, "split": 1, "fused": 2, "lift": 3, "sync15": 4}
 SCAN_ORDERS = {"sequential": 0, "kogge_stone": 1}
 
 
@@ -173,6 +174,15 @@ def rnea(robot, q, qd, qdd, V0=None, Vd0=None, Ftip=None, g=None,
     if full:
         return tau, dict(V=V, Vd=Vd, F=F, Fhat=Fh)
     return tau
+
+
+def eq15_operator(robot1, q, qd, qdd):
+    """The 28x28 operator A_i of Eq. (15) (x = (Vdot, Q, V, Fhat, 1)) of a 1-link robot."""
+    n, M, S, J = _robot(robot1)
+    assert n == 1
+    out = np.zeros((28, 28))
+    _check(lib().orc_eq15_operator(_p(M), _p(S), _p(J), float(q), float(qd), float(qdd), _p(out)))
+    return out
 
 
 def jsi(robot, q):

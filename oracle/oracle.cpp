@@ -485,6 +485,164 @@ IdOut rnea_scan_lift(const Chain& c, const double* q, const double* qd, const do
   return o;
 }
 
+// Synchronous forward scan of Eq. (15): x_i = A_i x_{i-1} on the
+// 28-vector x = (Vdot, Q, V, Fhat, 1), Q = (w x v, w1^2, w1w2, w1w3, w2^2, w2w3, w3^2)
+// (P:218).  The paper prints only the block pattern; the starred blocks (reading
+// A6) follow from Eq. (1) and P:217 for f = f_{i-1,i} = (R, p), s = S_i qd_i,
+// a = S_i qdd_i, X = Ad_{f^-1}:
+//   V'    = X V + s
+//   Vdot' = X Vdot + a + ad_{V'} s = X Vdot - ad_s X V + a            (ad_s s = 0)
+//   w' = R^T w + s_w,  v' = R^T (v + w x p) + s_v, so
+//   w' x v' = R^T (w x v) + R^T (w x (w x p)) + [s_w] R^T v
+//             + (-[s_v] R^T - [s_w] R^T [p]) w + s_w x s_v
+//   w'_a w'_b = (R^T w)_a (R^T w)_b + (R^T w)_a s_w,b + s_w,a (R^T w)_b + s_w,a s_w,b
+//   Fhat' = J Vdot' - ad^T_{V'} J V' = J Vdot' + H Q(V'),
+//   H Q = (m (w x v) + w x (w x h),  h x (w x v) + w x (I_o w))   (J = [[m, -[h]], [[h], I_o]])
+// (the 9-of-21 claim of P:218).  Every quadratic term is a fixed linear map of
+// the ww entries, so A_i is affine with the printed zero blocks (pinned against a
+// least-squares fit and against the recursion in tests/).  F_0 = 0 is
+// read as: the Fhat entry of the seed is unused (no row reads it).
+namespace eq15 {
+constexpr int Vd = 0, Q = 6, V = 15, F = 21, ONE = 27, D = 28;
+int widx(int j, int k) {                    // position of w_j w_k among (11, 12, 13, 22, 23, 33)
+  if (j > k) std::swap(j, k);
+  static const int tab[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+  return tab[j][k];
+}
+// coefficients of w x (w x x) on the ww entries: w (w.x) - x |w|^2
+void G(const V3& x, double out[3][6]) {
+  for (int k = 0; k < 3; ++k) for (int e = 0; e < 6; ++e) out[k][e] = 0;
+  for (int k = 0; k < 3; ++k)
+    for (int j = 0; j < 3; ++j) {
+      out[k][widx(k, j)] += x[j];
+      out[k][widx(j, j)] -= x[k];
+    }
+}
+double eps(int a, int b, int c) { return (double)((a - b) * (b - c) * (c - a)) / 2.0; }   // Levi-Civita
+}  // namespace eq15
+
+Dense eq15_operator(const M4& f, const V6& s, const V6& a, const M6& J) {
+  using namespace eq15;
+  Dense A(D * D, 0.0);
+  const M6 X = Ad(inv4(f));
+  M3 Rt{}, P{};
+  V3 p{}, sv{}, sw{};
+  for (int i = 0; i < 3; ++i) {
+    p[i] = f[i][3];
+    sv[i] = s[i];
+    sw[i] = s[3 + i];
+    for (int j = 0; j < 3; ++j) Rt[i][j] = f[j][i];
+  }
+  P = skew(p);
+  const M3 Ssv = skew(sv), Ssw = skew(sw);
+  // V' = X V + s
+  for (int r = 0; r < 6; ++r) {
+    for (int c = 0; c < 6; ++c) A[D * (V + r) + V + c] = X[r][c];
+    A[D * (V + r) + ONE] = s[r];
+  }
+  // Vdot' = X Vdot - ad_s X V + a
+  const M6 adsX = mul6(ad(s), X);
+  for (int r = 0; r < 6; ++r) {
+    for (int c = 0; c < 6; ++c) {
+      A[D * (Vd + r) + Vd + c] = X[r][c];
+      A[D * (Vd + r) + V + c] = -adsX[r][c];
+    }
+    A[D * (Vd + r) + ONE] = a[r];
+  }
+  // Q'[0:3] = w' x v'
+  double Gp[3][6];
+  G(p, Gp);
+  const M3 SswRt = mul3(Ssw, Rt), SsvRt = mul3(Ssv, Rt), SswRtP = mul3(SswRt, P);
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) A[D * (Q + r) + Q + c] = Rt[r][c];                 // R^T (w x v)
+    for (int e = 0; e < 6; ++e) {                                                   // R^T (w x (w x p))
+      double acc = 0;
+      for (int k = 0; k < 3; ++k) acc += Rt[r][k] * Gp[k][e];
+      A[D * (Q + r) + Q + 3 + e] = acc;
+    }
+    for (int c = 0; c < 3; ++c) {
+      A[D * (Q + r) + V + c] = SswRt[r][c];                                         // [s_w] R^T v
+      A[D * (Q + r) + V + 3 + c] = -SsvRt[r][c] - SswRtP[r][c];                     // (-[s_v]R^T - [s_w]R^T[p]) w
+    }
+  }
+  const V3 swxsv = {sw[1] * sv[2] - sw[2] * sv[1], sw[2] * sv[0] - sw[0] * sv[2], sw[0] * sv[1] - sw[1] * sv[0]};
+  for (int r = 0; r < 3; ++r) A[D * (Q + r) + ONE] = swxsv[r];
+  // Q'[3:9] = w'_a w'_b
+  for (int a_ = 0; a_ < 3; ++a_)
+    for (int b_ = a_; b_ < 3; ++b_) {
+      const int row = Q + 3 + widx(a_, b_);
+      for (int j = 0; j < 3; ++j)
+        for (int k = 0; k < 3; ++k) A[D * row + Q + 3 + widx(j, k)] += Rt[a_][j] * Rt[b_][k];
+      for (int j = 0; j < 3; ++j) A[D * row + V + 3 + j] = Rt[a_][j] * sw[b_] + sw[a_] * Rt[b_][j];
+      A[D * row + ONE] = sw[a_] * sw[b_];
+    }
+  // H: Q -> -ad^T_V J V
+  const double m = J[0][0];
+  const V3 h = {J[5][1], J[3][2], J[4][0]};
+  M3 Io{};
+  for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) Io[i][j] = J[3 + i][3 + j];
+  double H[6][9] = {};
+  double Gh[3][6];
+  G(h, Gh);
+  const M3 Sh = skew(h);
+  for (int k = 0; k < 3; ++k) {
+    H[k][k] = m;
+    for (int e = 0; e < 6; ++e) H[k][3 + e] = Gh[k][e];
+    for (int c = 0; c < 3; ++c) H[3 + k][c] = Sh[k][c];
+    for (int a_ = 0; a_ < 3; ++a_)
+      for (int b_ = 0; b_ < 3; ++b_)
+        for (int c = 0; c < 3; ++c) H[3 + k][3 + widx(a_, c)] += eps(k, a_, b_) * Io[b_][c];
+  }
+  // Fhat' = J (Vdot' row) + H (Q' row)
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < D; ++c) {
+      double acc = 0;
+      for (int k = 0; k < 6; ++k) acc += J[r][k] * A[D * (Vd + k) + c];
+      for (int k = 0; k < 9; ++k) acc += H[r][k] * A[D * (Q + k) + c];
+      A[D * (F + r) + c] = acc;
+    }
+  A[D * ONE + ONE] = 1.0;
+  return A;
+}
+
+IdOut rnea_scan_sync15(const Chain& c, const double* q, const double* qd, const double* qdd,
+                       const V6& V0, const V6& Vd0, const V6& Ftip, int order) {
+  using namespace eq15;
+  const int n = c.n;
+  IdOut o;
+  o.tau.assign(n, 0.0); o.V.assign(n, zv6()); o.Vd.assign(n, zv6());
+  o.F.assign(n, zv6()); o.Fhat.assign(n, zv6());
+  std::vector<M4> f = calc_transform(c, q);
+  // seed: constant map to x_0 = (Vdot_0, Q(V_0), V_0, 0, 1)
+  Dense seed(D * D, 0.0);
+  {
+    double x0[D] = {};
+    for (int k = 0; k < 6; ++k) { x0[Vd + k] = Vd0[k]; x0[V + k] = V0[k]; }
+    const double v[3] = {V0[0], V0[1], V0[2]}, w[3] = {V0[3], V0[4], V0[5]};
+    x0[Q + 0] = w[1] * v[2] - w[2] * v[1];
+    x0[Q + 1] = w[2] * v[0] - w[0] * v[2];
+    x0[Q + 2] = w[0] * v[1] - w[1] * v[0];
+    for (int a_ = 0; a_ < 3; ++a_)
+      for (int b_ = a_; b_ < 3; ++b_) x0[Q + 3 + widx(a_, b_)] = w[a_] * w[b_];
+    x0[ONE] = 1.0;
+    for (int r = 0; r < D; ++r) seed[D * r + ONE] = x0[r];
+  }
+  std::vector<Dense> a;
+  a.push_back(seed);
+  for (int i = 0; i < n; ++i) a.push_back(eq15_operator(f[i], scalev(c.S[i], qd[i]), scalev(c.S[i], qdd[i]), c.J[i]));
+  std::function<Dense(const Dense&, const Dense&)> comb =
+      [](const Dense& earlier, const Dense& later) { return dmul(later, earlier, D); };
+  std::vector<Dense> P = run_scan<Dense>(order, a, comb);
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < 6; ++k) {
+      o.Vd[i][k] = P[i + 1][D * (Vd + k) + ONE];
+      o.V[i][k] = P[i + 1][D * (V + k) + ONE];
+      o.Fhat[i][k] = P[i + 1][D * (F + k) + ONE];
+    }
+  force_scan_and_torque(c, f, Ftip, order, o);
+  return o;
+}
+
 // --------------------------------------------- forward dynamics, Eq. (4)-(8)
 V6 gravity_vd0(const double* g) { V6 a = zv6(); a[0] = -g[0]; a[1] = -g[1]; a[2] = -g[2]; return a; }
 
@@ -818,7 +976,7 @@ void orc_velacc_lift13(const double* a, double* out) { velacc_lift13(load_va(a),
 
 // Single-state RNEA (Eq. 1-2) with the full signature of Eq. (3).
 // variant: 0 serial recursion; 1 Alg. 1 split scans; 2 fused Eq. (13) scan;
-// 3 dense lifts Eq. (12)/(16).  order: 0 sequential fold, 1 Kogge-Stone.
+// 3 dense lifts Eq. (12)/(16); 4 synchronous Eq. (15) scan.  order: 0 sequential fold, 1 Kogge-Stone.
 // Optional outputs (may be NULL): V, Vd, F, Fhat as [n][6].
 int orc_rnea(int n, const double* M, const double* S, const double* J,
              const double* q, const double* qd, const double* qdd,
@@ -834,6 +992,7 @@ int orc_rnea(int n, const double* M, const double* S, const double* J,
     else if (variant == 1) o = rnea_scan_split(c, q, qd, qdd, v0, vd0, ft, order);
     else if (variant == 2) o = rnea_scan_fused(c, q, qd, qdd, v0, vd0, ft, order);
     else if (variant == 3) o = rnea_scan_lift(c, q, qd, qdd, v0, vd0, ft);
+    else if (variant == 4) o = rnea_scan_sync15(c, q, qd, qdd, v0, vd0, ft, order);
     else throw std::runtime_error("unknown variant");
     for (int i = 0; i < n; ++i) {
       tau[i] = o.tau[i];
@@ -842,6 +1001,17 @@ int orc_rnea(int n, const double* M, const double* S, const double* J,
       if (F) storev(o.F[i], F + 6 * i);
       if (Fhat) storev(o.Fhat[i], Fhat + 6 * i);
     }
+  });
+}
+
+// The 28x28 operator A_i of Eq. (15) for ONE link (n = 1 chain) at (q, qd, qdd).
+int orc_eq15_operator(const double* M, const double* S, const double* J, double q, double qd, double qdd,
+                      double* out) {
+  return guarded([&] {
+    Chain c = make_chain(1, M, S, J);
+    std::vector<M4> f = calc_transform(c, &q);
+    Dense A = eq15_operator(f[0], scalev(c.S[0], qd), scalev(c.S[0], qdd), c.J[0]);
+    for (int i = 0; i < 28 * 28; ++i) out[i] = A[i];
   });
 }
 
