@@ -60,9 +60,12 @@ typedef enum {
                              sweep re-derives V, Vdot by inverting the forward maps */
   RD_STRAT_BLOCK_SCAN = 5, /* one CTA per state, thread = link, CTA-wide scans: the single-robot latency
                               mode for long chains (n <= 512) */
-  RD_STRAT_WARP_SCAN_EQ13 = 6 /* the paper's operators literally: warp per state, one Eq. (13) semigroup scan
-                                 for V and Vdot (Eq. 12) and the Eq. (16) affine backward scan, body frame;
-                                 n <= 32 */
+  RD_STRAT_WARP_SCAN_EQ13 = 6, /* the paper's operators literally: warp per state, one Eq. (13) semigroup scan
+                                  for V and Vdot (Eq. 12) and the Eq. (16) affine backward scan, body frame;
+                                  n <= 32 */
+  RD_STRAT_WARP_SCAN_EQ15 = 7  /* the synchronous Eq. (15) scan literally: warp per state, one scan of the
+                                  28x28 operators on (Vdot, Q, V, Fhat, 1) (starred blocks: reading A6),
+                                  then the Eq. (16) backward scan; n <= 32; slow (one warp per SM) */
 } rd_strategy_t;
 
 /* Forward-dynamics algorithm. */

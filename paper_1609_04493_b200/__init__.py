@@ -25,7 +25,7 @@ __all__ = ["Model", "inverse_dynamics", "forward_dynamics", "inverse_dynamics_ho
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librd.so")
 
 STRATEGIES = {"auto": 0, "thread": 1, "warp_scan": 2, "generic": 3, "reverse": 4, "block_scan": 5,
-              "warp_scan_eq13": 6}
+              "warp_scan_eq13": 6, "warp_scan_eq15": 7}
 _STRAT_NAMES = {v: k for k, v in STRATEGIES.items()}
 FD_ALGOS = {"aba": 0, "jsiia": 1, "aba_scan": 2, "aba_merged": 3}
 

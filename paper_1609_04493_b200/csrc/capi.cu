@@ -408,6 +408,7 @@ rd_strategy_t resolve(rd_model_t m, int64_t batch, bool fp64) {
     case RD_STRAT_REVERSE: return m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
     case RD_STRAT_BLOCK_SCAN: return m->n <= 512 ? RD_STRAT_BLOCK_SCAN : RD_STRAT_GENERIC;
     case RD_STRAT_WARP_SCAN_EQ13: return warp_ok ? RD_STRAT_WARP_SCAN_EQ13 : RD_STRAT_GENERIC;
+    case RD_STRAT_WARP_SCAN_EQ15: return warp_ok ? RD_STRAT_WARP_SCAN_EQ15 : RD_STRAT_GENERIC;
     default: break;
   }
   if (warp_ok && batch <= kWarpScanMaxBatch) return RD_STRAT_WARP_SCAN;
@@ -437,6 +438,11 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   if (strat == RD_STRAT_WARP_SCAN_EQ13) {
     bool ok = false;
     e = rd::launch_rnea_warp13<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok);
+    if (!ok) strat = RD_STRAT_GENERIC;
+  }
+  if (strat == RD_STRAT_WARP_SCAN_EQ15) {
+    bool ok = false;
+    e = rd::launch_rnea_warp15<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok);
     if (!ok) strat = RD_STRAT_GENERIC;
   }
   if (strat == RD_STRAT_BLOCK_SCAN) {
@@ -707,7 +713,7 @@ int32_t rd_model_n(rd_model_t m) { return m ? m->n : -1; }
 
 rd_status_t rd_model_set_strategy(rd_model_t m, rd_strategy_t s) {
   if (!m) return fail(RD_E_ARG, "null model");
-  if (s < RD_STRAT_AUTO || s > RD_STRAT_WARP_SCAN_EQ13) return fail(RD_E_ARG, "unknown strategy");
+  if (s < RD_STRAT_AUTO || s > RD_STRAT_WARP_SCAN_EQ15) return fail(RD_E_ARG, "unknown strategy");
   m->strategy = s;
   return RD_OK;
 }

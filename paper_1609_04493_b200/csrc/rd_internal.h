@@ -88,6 +88,10 @@ cudaError_t launch_rnea_warp13(int n, const LinkConst<T>* L_dev, const Boundary<
                                int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
                                cudaStream_t st, int* launches, bool* supported);
 template <typename T>
+cudaError_t launch_rnea_warp15(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
+                               int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
+                               cudaStream_t st, int* launches, bool* supported);
+template <typename T>
 cudaError_t launch_rnea_block(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                               int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
                               cudaStream_t st, int* launches, bool* supported);

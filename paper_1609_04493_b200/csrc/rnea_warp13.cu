@@ -158,42 +158,7 @@ rnea_warp13_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T>
 #pragma unroll
       for (int k = 0; k < 6; ++k) Fh[k] = 0;
     }
-    // Eq. (16) operator of link l: F_l = L_l F_{l+1} + Fhat_l with L_l = Ad^T_{f_{l+1}^{-1}}
-    // = [[R', 0], [[p']R', R']] from link l+1's (R', p'); link n-1: F_{n-1} = Fhat + F_{n+1}.
-    const unsigned f = 0xffffffffu;
-    const T nR[9] = {__shfl_down_sync(f, R.r00, 1), __shfl_down_sync(f, R.r01, 1), __shfl_down_sync(f, R.r02, 1),
-                     __shfl_down_sync(f, R.r10, 1), __shfl_down_sync(f, R.r11, 1), __shfl_down_sync(f, R.r12, 1),
-                     __shfl_down_sync(f, R.r20, 1), __shfl_down_sync(f, R.r21, 1), __shfl_down_sync(f, R.r22, 1)};
-    const T np0 = __shfl_down_sync(f, p0, 1), np1 = __shfl_down_sync(f, p1, 1), np2 = __shfl_down_sync(f, p2, 1);
-    T Lm[36], bv[6];
-    const bool has_child = lane + 1 < n;
-#pragma unroll
-    for (int i = 0; i < 36; ++i) Lm[i] = 0;
-    if (has_child) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          Lm[6 * i + j] = nR[3 * i + j];
-          Lm[6 * (3 + i) + 3 + j] = nR[3 * i + j];
-        }
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const T x0 = nR[j], x1 = nR[3 + j], x2 = nR[6 + j];
-        Lm[6 * 3 + j] = np1 * x2 - np2 * x1;
-        Lm[6 * 4 + j] = np2 * x0 - np0 * x2;
-        Lm[6 * 5 + j] = np0 * x1 - np1 * x0;
-      }
-    } else if (!act) {
-#pragma unroll
-      for (int i = 0; i < 6; ++i) Lm[7 * i] = 1;        // padding lanes: identity operator
-    }
-#pragma unroll
-    for (int k = 0; k < 6; ++k) bv[k] = Fh[k] + ((lane == n - 1) ? bnd.Ftip[k] : T(0));
-#pragma unroll
-    for (int dd = 1; dd < 32; dd <<= 1) compose_shfl<T, true>(Lm, bv, dd, lane + dd < 32);
-    // tau_l = S_l^T F_l
-    const T t = fma(C.beta, bv[2], C.alpha * bv[5]);
+    const T t = eq16_backward_torque(lane, n, act, R, p0, p1, p2, Fh, bnd.Ftip, C.alpha, C.beta);
     if (act) tau[(int64_t)lane * B + b] = t;
   }
 }

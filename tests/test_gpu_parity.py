@@ -80,7 +80,8 @@ def test_C3_full_size_sampled(rd, dtype):
     check_id(rd, synth.robot_for(cfg), cfg["gravity"], q, qd, qdd, dtype, sample=sample)
 
 
-@pytest.mark.parametrize("strategy", ["thread", "generic", "warp_scan", "reverse", "warp_scan_eq13"])
+@pytest.mark.parametrize("strategy", ["thread", "generic", "warp_scan", "reverse", "warp_scan_eq13",
+                                      "warp_scan_eq15"])
 def test_C3_small_all_states(rd, strategy):
     cfg = synth.CONFIGS["C3"]
     q, qd, qdd = synth.states(cfg["seed"], 30, 0, 3000, cfg["ranges"])
@@ -92,7 +93,7 @@ def test_C3_small_all_states(rd, strategy):
 def test_ragged_batches(rd, B):
     r = synth.random_chain(30, 1030)
     q, qd, qdd = synth.states(7, 30, 0, B)
-    for strat in ("auto", "thread", "warp_scan", "generic", "reverse", "warp_scan_eq13"):
+    for strat in ("auto", "thread", "warp_scan", "generic", "reverse", "warp_scan_eq13", "warp_scan_eq15"):
         check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strat)
 
 
@@ -106,7 +107,7 @@ def test_empty_batch_is_noop(rd):
 def test_link_counts_random_chains(rd, n):
     r = synth.random_chain(n, 500 + n)
     q, qd, qdd = synth.states(11, n, 0, 777)
-    for strat in ("auto", "generic", "reverse", "thread", "block_scan") + (("warp_scan", "warp_scan_eq13") if n <= 32 else ()):
+    for strat in ("auto", "generic", "reverse", "thread", "block_scan") + (("warp_scan", "warp_scan_eq13", "warp_scan_eq15") if n <= 32 else ()):
         check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strat)
 
 
@@ -119,7 +120,7 @@ def test_prismatic_and_screw_joints_generic(rd, dtype):
             r["S"][i, :3] += 0.2 * r["S"][i, 3:]
             break
     q, qd, qdd = synth.states(12, 12, 0, 2000)
-    for strat in ("generic", "warp_scan", "warp_scan_eq13"):
+    for strat in ("generic", "warp_scan", "warp_scan_eq13", "warp_scan_eq15"):
         check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype, strategy=strat)
 
 
@@ -140,7 +141,7 @@ def test_full_boundary_V0_Vdot0_Ftip(rd):
     model = rd.Model.from_robot(r, (0, 0, 0))
     model.set_boundary(V0, Vd0, Ft)
     q, qd, qdd = synth.states(13, 7, 0, 300)
-    for strat in ("generic", "warp_scan", "warp_scan_eq13"):
+    for strat in ("generic", "warp_scan", "warp_scan_eq13", "warp_scan_eq15"):
         model.set_strategy(strat)
         tau = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd)).cpu().numpy()
         ref = np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b], V0, Vd0, Ft) for b in range(300)], 1)
