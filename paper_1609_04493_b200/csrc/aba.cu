@@ -28,6 +28,9 @@
 
 namespace rd {
 
+#ifndef RD_ABA_WSPF
+#define RD_ABA_WSPF 2
+#endif
 constexpr int kAbaPerLink = 7;   // Ubar = U/D (6), ubar = u/D
 constexpr int kAbaThreads = 128;
 int aba_ws_per_link() { return kAbaPerLink; }
@@ -273,16 +276,42 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
     for (int k = 0; k < 6; ++k) { a[k] = bnd.Vd0[k]; V[k] = bnd.V0[k]; }
     {
       T cq3 = __ldg(pq), cqd3 = __ldg(pqd);
+#if RD_ABA_WSPF
+      // (Ubar, ubar) of links i .. i+WSPF-1 in flight: the workspace reads come from
+      // DRAM (it does not fit in L2) and a sweep-3 step is short
+      constexpr int PD = RD_ABA_WSPF;
+      T cU[PD][7];
+#pragma unroll
+      for (int j = 0; j < PD; ++j)
+#pragma unroll
+        for (int k = 0; k < 7; ++k) cU[j][k] = ws[((int64_t)min(j, n - 1) * kAbaPerLink + k) * slots + slot];
+#endif
 #pragma unroll 2
       for (int i = 0; i < n; ++i) {
         const int64_t o = (int64_t)min(i + 1, n - 1) * B;
         const T nq3 = __ldg(pq + o), nqd3 = __ldg(pqd + o);
         const LinkDH<T>& C = L[i];
+#if RD_ABA_WSPF
+        T Ub[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) Ub[k] = cU[0][k];
+        const T ub = cU[0][6];
+#pragma unroll
+        for (int j = 0; j + 1 < PD; ++j)
+#pragma unroll
+          for (int k = 0; k < 7; ++k) cU[j][k] = cU[j + 1][k];
+        {
+          const T* wn = ws + (int64_t)min(i + PD, n - 1) * kAbaPerLink * slots + slot;
+#pragma unroll
+          for (int k = 0; k < 7; ++k) cU[PD - 1][k] = wn[k * slots];
+        }
+#else
         const T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
         T Ub[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) Ub[k] = w[k * slots];
         const T ub = w[6 * slots];
+#endif
         T s, c;
         dh_sincos(C, cq3, &s, &c);
         const T qdi = cqd3;

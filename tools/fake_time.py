@@ -1,13 +1,33 @@
-import os, sys
+"""A/B timing of one library build: python tools/fake_time.py LIB.so [--config C3] [--fd] [--strategy thread]
+[--dtype f64].  Median CUDA-event time of the call over 50 reps (quick_time.time_call)."""
+import argparse
+import os
+import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import paper_1609_04493_b200 as rd
-if len(sys.argv) > 1:
-    rd.LIB_PATH = sys.argv[1]
-import torch, numpy as np, synth
-from quick_time import time_call
-cfg = synth.CONFIGS["C3"]
-q, qd, qdd = synth.states(cfg["seed"], 30, 0, 1_000_000)
-tq, tqd, tqdd = (torch.from_numpy(x).cuda() for x in (q, qd, qdd))
-m = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"]); m.set_strategy("thread")
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import paper_1609_04493_b200 as rd  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("lib")
+ap.add_argument("--config", default="C3")
+ap.add_argument("--fd", action="store_true")
+ap.add_argument("--strategy", default="thread")
+ap.add_argument("--fd-algo", default="aba")
+ap.add_argument("--dtype", default="f64")
+a = ap.parse_args()
+rd.LIB_PATH = a.lib
+import torch  # noqa: E402
+import synth  # noqa: E402
+from quick_time import time_call  # noqa: E402
+
+cfg = synth.CONFIGS[a.config]
+n = cfg["n"]
+dt = torch.float64 if a.dtype == "f64" else torch.float32
+q, qd, qdd = synth.states(cfg["seed"], n, 0, cfg["batch"], cfg["ranges"])
+tq, tqd, tqdd = (torch.from_numpy(x).to("cuda", dt) for x in (q, qd, qdd))
+m = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
+m.set_strategy(a.strategy)
+m.set_fd_algo(a.fd_algo)
 out = torch.empty_like(tq)
-print(rd.LIB_PATH, f"{time_call(lambda: rd.inverse_dynamics(m, tq, tqd, tqdd, out), reps=50):.4f} ms")
+f = (lambda: rd.forward_dynamics(m, tq, tqd, tqdd, out)) if a.fd else (lambda: rd.inverse_dynamics(m, tq, tqd, tqdd, out))
+print(os.path.basename(a.lib), a.config, "fd" if a.fd else "id", f"{time_call(f, reps=50):.4f} ms")
