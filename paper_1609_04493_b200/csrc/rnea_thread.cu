@@ -118,14 +118,35 @@ template <> struct TmemIO<float> {
 // write of the new tile needs.  Every steady-state
 // step is ONE basic block (no branch between the two sweeps), so ptxas can
 // interleave them; the slot kind (TMEM or shared) is fixed per loop segment.
-#ifndef RD_PD
-#define RD_PD 2
+// Input prefetch distance (links, in stream order over tiles) and unroll factor
+// of the steady-state step loops, per precision.  Unrolling by a divisor of the
+// distance lets ptxas keep the in-flight loads in fixed registers instead of
+// rotating them with MOVs that wait on the loads at every loop head (ncu: those
+// MOVs and the back-edge carried ~20 % long-scoreboard stalls).  Measured on
+// B200: fp64 n = 30 (W = 8), 1M states 0.543 -> 0.494 ms with
+// (8, 4); fp32 n = 30 (W = 16) 0.312 -> 0.309 ms with (4, 2); the 16-warp fp64
+// plan (n <= 15, 128-register cap) keeps (2, 1).
+#ifndef RD_PD64
+#define RD_PD64 8
 #endif
-constexpr int kPD = RD_PD;   // input prefetch distance (links, stream order over tiles)
+#ifndef RD_U64
+#define RD_U64 4
+#endif
+#ifndef RD_PD32
+#define RD_PD32 4
+#endif
+#ifndef RD_U32
+#define RD_U32 2
+#endif
+template <typename T, int W> struct StepCfg { static constexpr int kPD = 2, kUnroll = 1; };
+template <> struct StepCfg<double, 8> { static constexpr int kPD = RD_PD64, kUnroll = RD_U64; };
+template <> struct StepCfg<float, 8> { static constexpr int kPD = RD_PD32, kUnroll = RD_U32; };
+template <> struct StepCfg<float, 16> { static constexpr int kPD = RD_PD32, kUnroll = RD_U32; };
 
-template <typename T>
+template <typename T, int PD>
 struct FwdState {
   T V[6], Vd[6];
+  static constexpr int kPD = PD;
   T a_q[kPD], a_qd[kPD], a_qa[kPD];    // inputs of the next kPD links in stream order ([0] = current)
   const T *pq, *pqd, *pqa;              // this tile's column
   const T *xq, *xqd, *xqa;              // the next tile's column (prefetch across the tile boundary)
@@ -141,8 +162,8 @@ struct BwdState {
 // Inputs are consumed as ONE stream over (tile, link): the loads issued at link
 // k fetch link k+2 of this tile, or link k+2-n of the NEXT tile, so the first
 // links of a tile are already in registers when its forward sweep starts.
-template <typename T>
-__device__ __forceinline__ void fwd_init(FwdState<T>& f, const ThreadParams<T>& P, int64_t B, int64_t bl,
+template <typename T, int PD>
+__device__ __forceinline__ void fwd_init(FwdState<T, PD>& f, const ThreadParams<T>& P, int64_t B, int64_t bl,
                                          int64_t bl_next, const T* q, const T* qd, const T* qdd, bool first) {
 #pragma unroll
   for (int k = 0; k < 6; ++k) { f.V[k] = P.bnd.V0[k]; f.Vd[k] = P.bnd.Vd0[k]; }
@@ -150,7 +171,7 @@ __device__ __forceinline__ void fwd_init(FwdState<T>& f, const ThreadParams<T>& 
   f.xq = q + bl_next; f.xqd = qd + bl_next; f.xqa = qdd + bl_next;
   if (first) {
 #pragma unroll
-    for (int j = 0; j < kPD; ++j) {
+    for (int j = 0; j < PD; ++j) {
       const bool here = j < P.n;
       const int64_t off = (int64_t)(here ? j : min(j - P.n, P.n - 1)) * B;   // n < kPD: reloaded per tile
       f.a_q[j] = __ldg((here ? f.pq : f.xq) + off);
@@ -166,13 +187,14 @@ __device__ __forceinline__ void bwd_init(BwdState<T>& g, const ThreadParams<T>& 
   g.ca = 1; g.sa = 0; g.p0 = g.p1 = g.p2 = 0; g.s = 0; g.c = 1;   // f_{n,n+1} = I (A5)
 }
 // forward link k: V_k, Vdot_k, Fhat_k -> st[8]
-template <typename T>
-__device__ __forceinline__ void fwd_link(FwdState<T>& f, const ThreadParams<T>& P, int64_t B, int k, T* st) {
+template <typename T, int PD>
+__device__ __forceinline__ void fwd_link(FwdState<T, PD>& f, const ThreadParams<T>& P, int64_t B, int k, T* st) {
   const int n = P.n;
   // this link's inputs (loaded two links earlier) and the loads for link k+2
   // (stream order over tiles).  (A variant that prefetched into L1 and loaded in
   // place was 20 % slower.)
   const T cq = f.a_q[0], cqd = f.a_qd[0], cqa = f.a_qa[0];
+  constexpr int kPD = PD;
   const int k2 = k + kPD;
   const bool here = k2 < n;
   const int64_t off2 = (int64_t)(here ? k2 : min(k2 - n, n - 1)) * B;   // n < kPD: reloaded per tile
@@ -269,7 +291,8 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
     }
   };
 
-  FwdState<T> f;
+  using Cfg = StepCfg<T, W>;
+  FwdState<T, Cfg::kPD> f;
   BwdState<T> g;
   g.b = 0;
   g.valid = false;
@@ -289,7 +312,7 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
       break;
     }
     const int64_t bn = b + (int64_t)gridDim.x * NT;
-    fwd_init(f, P, B, fvalid ? b : (B - 1), bn < B ? bn : (B - 1), q, qd, qdd, it == 0 || P.n < kPD);
+    fwd_init(f, P, B, fvalid ? b : (B - 1), bn < B ? bn : (B - 1), q, qd, qdd, it == 0 || P.n < Cfg::kPD);
     if (it == 0) {
       // prologue: forward of the first tile alone (parity 0: slot = link)
       for (int k = 0; k < n; ++k) {
@@ -314,6 +337,7 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
         if (k0 >= k1) return;
         typename TmemIO<T>::Regs r;
         TmemIO<T>::ld(tbase + (uint32_t)((bpar ? k0 : n - 1 - k0) * KC), r);
+#pragma unroll (Cfg::kUnroll)
         for (int k = k0; k < k1; ++k) {
           const int slot = bpar ? k : n - 1 - k;
           const int knx = min(k + 1, k1 - 1);
@@ -330,8 +354,10 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
       };
       if (bpar) {
         tmem_seg(0, lt);
+#pragma unroll (Cfg::kUnroll)
         for (int k = lt; k < n; ++k) smem_step(k);
       } else {
+#pragma unroll (Cfg::kUnroll)
         for (int k = 0; k < n - lt; ++k) smem_step(k);
         tmem_seg(n - lt, n);
       }
