@@ -138,6 +138,9 @@ template <> struct TmemIO<float> {
 #ifndef RD_U32
 #define RD_U32 2
 #endif
+#ifndef RD_TAU_DEFER
+#define RD_TAU_DEFER 1
+#endif
 template <typename T, int W> struct StepCfg { static constexpr int kPD = 2, kUnroll = 1; };
 template <> struct StepCfg<double, 8> { static constexpr int kPD = RD_PD64, kUnroll = RD_U64; };
 template <> struct StepCfg<float, 8> { static constexpr int kPD = RD_PD32, kUnroll = RD_U32; };
@@ -157,6 +160,10 @@ struct BwdState {
   T ca, sa, p0, p1, p2, s, c;   // DH constants and stashed (sin, cos) of the child link i+1
   int64_t b;
   bool valid;
+#if RD_TAU_DEFER
+  T tp;                         // tau of the previous backward link, stored one step later
+  int ip;                       // its link index (-1: none pending)
+#endif
 };
 
 // Inputs are consumed as ONE stream over (tile, link): the loads issued at link
@@ -181,7 +188,17 @@ __device__ __forceinline__ void fwd_init(FwdState<T, PD>& f, const ThreadParams<
   }
 }
 template <typename T>
+__device__ __forceinline__ void bwd_flush(BwdState<T>& g, int64_t B, T* __restrict__ tau) {
+#if RD_TAU_DEFER
+  if (g.valid && g.ip >= 0) tau[(int64_t)g.ip * B + g.b] = g.tp;
+  g.ip = -1;
+#endif
+}
+template <typename T>
 __device__ __forceinline__ void bwd_init(BwdState<T>& g, const ThreadParams<T>& P) {
+#if RD_TAU_DEFER
+  g.ip = -1;
+#endif
 #pragma unroll
   for (int k = 0; k < 6; ++k) g.F[k] = P.bnd.Ftip[k];
   g.ca = 1; g.sa = 0; g.p0 = g.p1 = g.p2 = 0; g.s = 0; g.c = 1;   // f_{n,n+1} = I (A5)
@@ -235,10 +252,20 @@ template <typename T>
 __device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& P, int64_t B, int i,
                                          const T* cur, T* __restrict__ tau) {
   T Fo[6];
+#if RD_TAU_DEFER
+  // the previous link's tau, whose DFMA chain finished a whole step ago (storing
+  // it right after the chain stalled the warp on the fixed-latency dependency)
+  if (g.valid && g.ip >= 0) tau[(int64_t)g.ip * B + g.b] = g.tp;
+#endif
   dh_bwd(g.ca, g.sa, g.p0, g.p1, g.p2, g.s, g.c, g.F, cur + 2, Fo);
 #pragma unroll
   for (int j = 0; j < 6; ++j) g.F[j] = Fo[j];
+#if RD_TAU_DEFER
+  g.tp = g.F[5];
+  g.ip = i;
+#else
   if (g.valid) tau[(int64_t)i * B + g.b] = g.F[5];
+#endif
   const LinkDH<T>& C = P.L[i];
   g.ca = C.ca; g.sa = C.sa; g.p0 = C.p0; g.p1 = C.p1; g.p2 = C.p2;
   g.s = cur[0]; g.c = cur[1];
@@ -296,6 +323,9 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
   BwdState<T> g;
   g.b = 0;
   g.valid = false;
+#if RD_TAU_DEFER
+  g.ip = -1;
+#endif
   for (int64_t it = 0; it <= my_tiles; ++it) {
     const int64_t b = (blockIdx.x + it * gridDim.x) * NT + tid;
     const bool fvalid = b < B;
@@ -309,6 +339,7 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
         get_any(bpar ? n - 1 - i : i, cur);
         bwd_link(g, P, B, i, cur, tau);
       }
+      bwd_flush(g, B, tau);
       break;
     }
     const int64_t bn = b + (int64_t)gridDim.x * NT;
@@ -363,6 +394,7 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
       }
     }
     tmem_wait_st();
+    bwd_flush(g, B, tau);
     g.b = b;
     g.valid = fvalid;
   }
