@@ -19,6 +19,17 @@
 namespace rd {
 
 constexpr int kRevThreads = 128;
+// Input prefetch distance (links) and unroll of both sweeps: unrolling by the
+// distance keeps the in-flight loads in fixed registers (no MOV rotation that
+// waits on them at every loop head); tau is stored one link late, off the end
+// of the backward DFMA chain (thread kernel).
+#ifndef RD_REV_PD
+#define RD_REV_PD 4
+#endif
+#ifndef RD_REV_U
+#define RD_REV_U 4
+#endif
+constexpr int kRevPD = RD_REV_PD, kRevU = RD_REV_U;
 
 template <typename T>
 __global__ void __launch_bounds__(kRevThreads, 4)
@@ -38,11 +49,22 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
 #pragma unroll
     for (int k = 0; k < 6; ++k) { V[k] = bnd.V0[k]; Vd[k] = bnd.Vd0[k]; }
     // ---- forward sweep, Eq. (1)
-    T nq = __ldg(pq), nqd = __ldg(pqd), nqa = __ldg(pqa);
+    constexpr int PD = kRevPD;
+    T aq[PD], aqd[PD], aqa[PD];
+#pragma unroll
+    for (int j = 0; j < PD; ++j) {
+      const int64_t o = (int64_t)min(j, n - 1) * B;
+      aq[j] = __ldg(pq + o); aqd[j] = __ldg(pqd + o); aqa[j] = __ldg(pqa + o);
+    }
+#pragma unroll (kRevU)
     for (int i = 0; i < n; ++i) {
-      const T qi = nq, qdi = nqd, qai = nqa;
-      const int64_t o = (int64_t)min(i + 1, n - 1) * B;
-      nq = __ldg(pq + o); nqd = __ldg(pqd + o); nqa = __ldg(pqa + o);
+      const T qi = aq[0], qdi = aqd[0], qai = aqa[0];
+#pragma unroll
+      for (int j = 0; j + 1 < PD; ++j) { aq[j] = aq[j + 1]; aqd[j] = aqd[j + 1]; aqa[j] = aqa[j + 1]; }
+      {
+        const int64_t o = (int64_t)min(i + PD, n - 1) * B;
+        aq[PD - 1] = __ldg(pq + o); aqd[PD - 1] = __ldg(pqd + o); aqa[PD - 1] = __ldg(pqa + o);
+      }
       const LinkDH<T> C = L[i];
       T s, c;
       if (sizeof(T) == 8) {
@@ -70,19 +92,29 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
 #pragma unroll
     for (int k = 0; k < 6; ++k) F[k] = bnd.Ftip[k];
     T ca = 1, sa = 0, p0 = 0, p1 = 0, p2 = 0, sn = 0, cn = 1;   // child transform (identity at the tip)
-    const int64_t on = (int64_t)(n - 1) * B;
-    nq = __ldg(pq + on); nqd = __ldg(pqd + on); nqa = __ldg(pqa + on);
+#pragma unroll
+    for (int j = 0; j < PD; ++j) {
+      const int64_t o = (int64_t)max(n - 1 - j, 0) * B;
+      aq[j] = __ldg(pq + o); aqd[j] = __ldg(pqd + o); aqa[j] = __ldg(pqa + o);
+    }
+    T tp = 0;                                   // tau of link i+1, stored during link i
+#pragma unroll (kRevU)
     for (int i = n - 1; i >= 0; --i) {
-      const T qi = nq, qdi = nqd, qai = nqa;
-      const int64_t o = (int64_t)max(i - 1, 0) * B;
-      nq = __ldg(pq + o); nqd = __ldg(pqd + o); nqa = __ldg(pqa + o);
+      const T qi = aq[0], qdi = aqd[0], qai = aqa[0];
+#pragma unroll
+      for (int j = 0; j + 1 < PD; ++j) { aq[j] = aq[j + 1]; aqd[j] = aqd[j + 1]; aqa[j] = aqa[j + 1]; }
+      {
+        const int64_t o = (int64_t)max(i - PD, 0) * B;
+        aq[PD - 1] = __ldg(pq + o); aqd[PD - 1] = __ldg(pqd + o); aqa[PD - 1] = __ldg(pqa + o);
+      }
+      if (i < n - 1) tau[(int64_t)(i + 1) * B + b] = tp;
       const LinkDH<T> C = L[i];
       T Fh[6], Fo[6];
       bias_force(C, V, Vd, Fh);
       dh_bwd(ca, sa, p0, p1, p2, sn, cn, F, Fh, Fo);
 #pragma unroll
       for (int k = 0; k < 6; ++k) F[k] = Fo[k];
-      tau[(int64_t)i * B + b] = F[5];
+      tp = F[5];
       T s, c;
       if (sizeof(T) == 8) {
         rd_sincos(qi + C.th0, &s, &c);
@@ -106,6 +138,7 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
       dh_ad_f(C, s, c, y, Vd);
       ca = C.ca; sa = C.sa; p0 = C.p0; p1 = C.p1; p2 = C.p2; sn = s; cn = c;
     }
+    tau[b] = tp;
   }
 }
 
