@@ -31,6 +31,21 @@ namespace rd {
 #ifndef RD_ABA_WSPF
 #define RD_ABA_WSPF 2
 #endif
+// Input prefetch distances / unroll factors of the DH kernel's sweeps 1 and 3
+// (short iterations; see rnea_thread.cu StepCfg for why unroll ~ distance).
+#ifndef RD_ABA_S1PD
+#define RD_ABA_S1PD 4
+#endif
+#ifndef RD_ABA_S1U
+#define RD_ABA_S1U 4
+#endif
+#ifndef RD_ABA_S3PD
+#define RD_ABA_S3PD 1
+#endif
+#ifndef RD_ABA_S3U
+#define RD_ABA_S3U 2
+#endif
+constexpr int kS1PD = RD_ABA_S1PD, kS1U = RD_ABA_S1U, kS3PD = RD_ABA_S3PD, kS3U = RD_ABA_S3U;
 constexpr int kAbaPerLink = 7;   // Ubar = U/D (6), ubar = u/D
 constexpr int kAbaThreads = 128;
 int aba_ws_per_link() { return kAbaPerLink; }
@@ -198,14 +213,23 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
     T V[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) V[k] = bnd.V0[k];
-    // sweep 1: V_n only; inputs two links ahead
+    // sweep 1: V_n only; inputs kS1PD links ahead
     {
-      T cq = __ldg(pq), cqd = __ldg(pqd);
-      T nq = __ldg(pq + (int64_t)min(1, n - 1) * B), nqd = __ldg(pqd + (int64_t)min(1, n - 1) * B);
-#pragma unroll 2
+      T aq[kS1PD], aqd[kS1PD];
+#pragma unroll
+      for (int j = 0; j < kS1PD; ++j) {
+        const int64_t o = (int64_t)min(j, n - 1) * B;
+        aq[j] = __ldg(pq + o); aqd[j] = __ldg(pqd + o);
+      }
+#pragma unroll (kS1U)
       for (int i = 0; i < n; ++i) {
-        const int64_t o = (int64_t)min(i + 2, n - 1) * B;
-        const T fq = __ldg(pq + o), fqd = __ldg(pqd + o);
+        const T cq = aq[0], cqd = aqd[0];
+#pragma unroll
+        for (int j = 0; j + 1 < kS1PD; ++j) { aq[j] = aq[j + 1]; aqd[j] = aqd[j + 1]; }
+        {
+          const int64_t o = (int64_t)min(i + kS1PD, n - 1) * B;
+          aq[kS1PD - 1] = __ldg(pq + o); aqd[kS1PD - 1] = __ldg(pqd + o);
+        }
         const LinkDH<T>& C = L[i];
         T s, c;
         dh_sincos(C, cq, &s, &c);
@@ -214,7 +238,6 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
         Vn[5] += cqd;
 #pragma unroll
         for (int k = 0; k < 6; ++k) V[k] = Vn[k];
-        cq = nq; cqd = nqd; nq = fq; nqd = fqd;
       }
     }
     Sym6<T> K, Kc;
@@ -275,7 +298,12 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
 #pragma unroll
     for (int k = 0; k < 6; ++k) { a[k] = bnd.Vd0[k]; V[k] = bnd.V0[k]; }
     {
-      T cq3 = __ldg(pq), cqd3 = __ldg(pqd);
+      T bq[kS3PD], bqd[kS3PD];
+#pragma unroll
+      for (int j = 0; j < kS3PD; ++j) {
+        const int64_t o = (int64_t)min(j, n - 1) * B;
+        bq[j] = __ldg(pq + o); bqd[j] = __ldg(pqd + o);
+      }
 #if RD_ABA_WSPF
       // (Ubar, ubar) of links i .. i+WSPF-1 in flight: the workspace reads come from
       // DRAM (it does not fit in L2) and a sweep-3 step is short
@@ -286,10 +314,15 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
 #pragma unroll
         for (int k = 0; k < 7; ++k) cU[j][k] = ws[((int64_t)min(j, n - 1) * kAbaPerLink + k) * slots + slot];
 #endif
-#pragma unroll 2
+#pragma unroll (kS3U)
       for (int i = 0; i < n; ++i) {
-        const int64_t o = (int64_t)min(i + 1, n - 1) * B;
-        const T nq3 = __ldg(pq + o), nqd3 = __ldg(pqd + o);
+        const T cq3 = bq[0], cqd3 = bqd[0];
+#pragma unroll
+        for (int j = 0; j + 1 < kS3PD; ++j) { bq[j] = bq[j + 1]; bqd[j] = bqd[j + 1]; }
+        {
+          const int64_t o = (int64_t)min(i + kS3PD, n - 1) * B;
+          bq[kS3PD - 1] = __ldg(pq + o); bqd[kS3PD - 1] = __ldg(pqd + o);
+        }
         const LinkDH<T>& C = L[i];
 #if RD_ABA_WSPF
         T Ub[6];
@@ -331,7 +364,6 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
         an[5] += qddi;
 #pragma unroll
         for (int k = 0; k < 6; ++k) { a[k] = an[k]; V[k] = Vn[k]; }
-        cq3 = nq3; cqd3 = nqd3;
       }
     }
   }
