@@ -17,7 +17,8 @@ for dt in (torch.float64, torch.float32):
         for B in (1, 37, 300):
             q, qd, qdd = (torch.from_numpy(x).to("cuda", dt) for x in synth.states(1, n, 0, B))
             skip = os.environ.get("SKIP_STRATS", "").split(",")
-            for strat in ("thread", "warp_scan", "generic", "reverse", "block_scan"):
+            for strat in ("thread", "warp_scan", "generic", "reverse", "block_scan", "warp_scan_eq13",
+                          "warp_scan_eq15"):
                 if strat in skip:
                     continue
                 model.set_strategy(strat)
@@ -28,5 +29,7 @@ for dt in (torch.float64, torch.float32):
                     continue
                 model.set_fd_algo(algo)
                 rd.forward_dynamics(model, q, qd, tau)
+                st = torch.empty(B, dtype=torch.int32, device="cuda")
+                rd.forward_dynamics(model, q, qd, tau, status=st)
 torch.cuda.synchronize()
 print("sanitize_run ok")
