@@ -80,6 +80,34 @@ def test_C3_full_size_sampled(rd, dtype):
     check_id(rd, synth.robot_for(cfg), cfg["gravity"], q, qd, qdd, dtype, sample=sample)
 
 
+def test_C5_full_size_sampled(rd):
+    # BASELINE config C5: 10^7 states on one GPU (the single-GPU bench workload of
+    # --config C5; 1.25M per GPU at 8 GPUs), the launch bench.py times.  Inputs are
+    # generated chunk by chunk straight into device memory; the oracle checks a
+    # sample: both ends, tile-boundary neighbourhoods and random states.
+    cfg = synth.CONFIGS["C5"]
+    n, B = cfg["n"], cfg["batch"]
+    tq, tqd, tqdd = (torch.empty((n, B), dtype=torch.float64, device="cuda") for _ in range(3))
+    chunk = 1_000_000
+    for b0 in range(0, B, chunk):
+        b1 = min(B, b0 + chunk)
+        for t, x in zip((tq, tqd, tqdd), synth.states(cfg["seed"], n, b0, b1, cfg["ranges"])):
+            t[:, b0:b1].copy_(torch.from_numpy(x))
+    model = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
+    assert model.resolve_strategy(B, True) == "thread"
+    tau = rd.inverse_dynamics(model, tq, tqd, tqdd)
+    rng = np.random.default_rng(99)
+    sample = np.unique(np.concatenate([np.arange(512), np.arange(B - 512, B), rng.integers(0, B, 4096),
+                                       np.arange(255, B, 256 * 9973), np.arange(256, B, 256 * 9973)]))
+    idx = torch.from_numpy(sample).cuda()
+    got = tau[:, idx].cpu().numpy()
+    q, qd, qdd = (t[:, idx].cpu().numpy() for t in (tq, tqd, tqdd))
+    ref = oracle.rnea_batch(synth.robot_for(cfg), cfg["gravity"], q, qd, qdd)
+    assert rel_err_per_state(got, ref).max() <= TOL[torch.float64]
+    del tq, tqd, tqdd, tau
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("strategy", ["thread", "generic", "warp_scan", "reverse", "warp_scan_eq13",
                                       "warp_scan_eq15"])
 def test_C3_small_all_states(rd, strategy):
