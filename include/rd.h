@@ -53,11 +53,13 @@ typedef enum {
 /* In-robot parallelisation strategy of the inverse-dynamics kernel (north_star (2)). */
 typedef enum {
   RD_STRAT_AUTO = 0,      /* chosen per (n, dtype, batch) from the measured table */
-  RD_STRAT_THREAD = 1,    /* one thread per state, serial recursion (stash in TMEM/registers) */
+  RD_STRAT_THREAD = 1,    /* one thread per state, serial recursion, per-link stash on chip (TMEM + shared
+                             memory); revolute (zero pitch) and prismatic joints, n <= 30 fp64 / 32 fp32;
+                             otherwise falls back to REVERSE (screw joints: GENERIC) */
   RD_STRAT_WARP_SCAN = 2, /* one warp per state, lane = link, Kogge-Stone shuffle scans */
   RD_STRAT_GENERIC = 3,   /* one thread per state, any n, any joints, stash in a global workspace */
-  RD_STRAT_REVERSE = 4,   /* one thread per state, any n (all-revolute chains), no stash: the backward
-                             sweep re-derives V, Vdot by inverting the forward maps */
+  RD_STRAT_REVERSE = 4,   /* one thread per state, any n (revolute / prismatic joints; screw: GENERIC),
+                             no stash: the backward sweep re-derives V, Vdot by inverting the forward maps */
   RD_STRAT_BLOCK_SCAN = 5, /* one CTA per state, thread = link, CTA-wide scans: the single-robot latency
                               mode for long chains (n <= 512) */
   RD_STRAT_WARP_SCAN_EQ13 = 6, /* the paper's operators literally: warp per state, one Eq. (13) semigroup scan

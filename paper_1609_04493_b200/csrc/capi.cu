@@ -142,7 +142,12 @@ struct rd_model_s {
   std::vector<rd::LinkConst<double>> L64;
   std::vector<rd::LinkConst<float>> L32;
   std::vector<Rigid> T;            // joint frame of link i expressed in the user's link-i frame
-  bool dh_ok = false;              // DH frames built (all revolute, zero pitch)
+  bool dh_ok = false;              // DH frames built (every joint revolute with zero pitch, or prismatic)
+  bool dh_eligible = false;        // no screw joints
+  std::vector<unsigned char> prism;  // per link: 1 = prismatic
+  bool has_prism = false;
+  uint32_t prism_mask = 0;         // bit i = prism[i] (links < 32)
+  unsigned char* dPrism = nullptr; // device copy of prism (REVERSE kernel)
   std::vector<rd::LinkDH<double>> D64;
   std::vector<rd::LinkDH<float>> D32;
   rd::LinkDH<double>* dD64 = nullptr;
@@ -201,7 +206,8 @@ void rebuild_boundary(rd_model_t m) {
   }
 }
 
-// Modified-DH (Craig) frames for an all-revolute chain, from the joint frames:
+// Modified-DH (Craig) frames for a chain of revolute (zero pitch) and prismatic
+// joints, from the joint frames (a prismatic joint slides along z_i: d = d0 + q):
 // G_i = pose of joint frame i in the base at q = 0 (z_i = joint axis).  Frame
 // D_i keeps z_i and puts its origin/x-axis on the common normal of axes i and
 // i+1 (any perpendicular for parallel axes; the joint frame itself for i = n);
@@ -389,12 +395,13 @@ template <> const rd::Boundary<float>& bnd<float>(rd_model_t m) { return m->b32;
 //  * batch <= kWarpScanMaxBatch and n <= 32 -> WARP_SCAN: one warp per state,
 //    lane = link, log-depth shuffle scans; the latency regime (paper P:505/P:524),
 //    e.g. n = 30, B = 1..1000: 21-24 us vs 43-49 us for THREAD;
-//  * otherwise THREAD when the on-chip stash fits (n <= 30 fp64 / 32 fp32, all
-//    joints revolute with zero pitch): 3.9x faster than WARP_SCAN at B = 1M;
+//  * otherwise THREAD when the on-chip stash fits (n <= 30 fp64 / 32 fp32, every
+//    joint revolute with zero pitch or prismatic): 3.9x faster than WARP_SCAN at B = 1M;
 //  * otherwise GENERIC (any n, any joint type).
 //  * 32 < n <= 512 and batch <= kBlockScanMaxBatch -> BLOCK_SCAN: one CTA per
 //    state (NEXT-3), e.g. n = 512, B = 1: 29 us vs 262 us (REVERSE), 687 us (GENERIC);
-//  * longer all-revolute chains at larger batch -> REVERSE (stash-free), else GENERIC.
+//  * longer revolute/prismatic chains at larger batch -> REVERSE (stash-free), else
+//    (screw joints) GENERIC.
 constexpr int64_t kWarpScanMaxBatch = 4096;
 constexpr int64_t kBlockScanMaxBatch = 1024;
 
@@ -428,7 +435,8 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   cudaError_t e = cudaSuccess;
   if (strat == RD_STRAT_THREAD) {
     bool ok = false;
-    e = rd::launch_rnea_thread<T>(m->n, dh_consts<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok);
+    e = rd::launch_rnea_thread<T>(m->n, dh_consts<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok,
+                                  m->prism_mask);
     if (!ok) strat = RD_STRAT_GENERIC;
   } else if (strat == RD_STRAT_WARP_SCAN) {
     bool ok = false;
@@ -451,7 +459,8 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     if (!ok) strat = RD_STRAT_GENERIC;
   }
   if (strat == RD_STRAT_REVERSE) {
-    e = rd::launch_rnea_rev<T>(m->n, dh_dev<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches);
+    e = rd::launch_rnea_rev<T>(m->n, dh_dev<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches,
+                               m->has_prism ? m->dPrism : nullptr);
   }
   if (strat == RD_STRAT_GENERIC) {
     std::lock_guard<std::mutex> lk(m->mu);
@@ -508,7 +517,7 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   st = ensure_ws(m, (size_t)slots * m->n * rd::aba_ws_per_link() * sizeof(T));
   if (st != RD_OK) return st;
   static const bool no_dh = getenv("RD_ABA_NODH") && getenv("RD_ABA_NODH")[0] == '1';   // A/B knob
-  cudaError_t e = (m->dh_ok && !no_dh)
+  cudaError_t e = (m->dh_ok && !m->has_prism && !no_dh)      // the DH ABA kernel is revolute-only
       ? rd::launch_aba_dh<T>(m->n, dh_dev<T>(m), dh_bnd<T>(m), batch, q, qd, tau, qdd,
                              reinterpret_cast<T*>(m->ws), slots, s, &g_launches, status)
       : rd::launch_aba<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
@@ -599,6 +608,8 @@ rd_status_t rd_model_create(int32_t n, const double* M, const double* S, const d
   m->L64.resize(n);
   m->L32.resize(n);
   m->all_revolute = true;
+  m->dh_eligible = true;
+  m->prism.assign(n, 0);
   std::vector<Rigid> Mps(n);
   std::vector<std::array<double, 36>> Jps(n);
   // Joint frames: T_i = (R_a, r) with R_a e_z = joint axis and r the point of
@@ -629,6 +640,13 @@ rd_status_t rd_model_create(int32_t n, const double* M, const double* S, const d
       beta = 1.0;
     }
     if (!(alpha == 1.0 && beta == 0.0)) m->all_revolute = false;
+    if (alpha == 0.0) {
+      m->prism[i] = 1;
+      m->has_prism = true;
+      if (i < 32) m->prism_mask |= 1u << i;
+    } else if (beta != 0.0) {
+      m->dh_eligible = false;                       // screw joint: no DH form with one variable
+    }
     m->T[i] = Ti;
     Rigid Tprev = (i == 0) ? rigid_identity() : m->T[i - 1];
     Rigid Mp = rigid_mul(rigid_mul(rigid_inv(Tprev), rigid_from4(M + 16 * i)), Ti);
@@ -674,7 +692,7 @@ rd_status_t rd_model_create(int32_t n, const double* M, const double* S, const d
     m->gravity[k] = gravity[k];
     m->Vd0[k] = -gravity[k];     // reading A3: Vdot_0 = (-g, 0)
   }
-  m->dh_ok = m->all_revolute && build_dh(m, Mps, Jps);
+  m->dh_ok = m->dh_eligible && build_dh(m, Mps, Jps);
   rebuild_boundary(m);
   cudaError_t e = cudaMalloc(&m->dL64, sizeof(rd::LinkConst<double>) * n);
   if (e == cudaSuccess) e = cudaMalloc(&m->dL32, sizeof(rd::LinkConst<float>) * n);
@@ -685,6 +703,8 @@ rd_status_t rd_model_create(int32_t n, const double* M, const double* S, const d
     if (e == cudaSuccess) e = cudaMalloc(&m->dD32, sizeof(rd::LinkDH<float>) * n);
     if (e == cudaSuccess) e = cudaMemcpy(m->dD64, m->D64.data(), sizeof(rd::LinkDH<double>) * n, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(m->dD32, m->D32.data(), sizeof(rd::LinkDH<float>) * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && m->has_prism) e = cudaMalloc(&m->dPrism, n);
+    if (e == cudaSuccess && m->has_prism) e = cudaMemcpy(m->dPrism, m->prism.data(), n, cudaMemcpyHostToDevice);
   }
   if (e != cudaSuccess) {
     rd_model_destroy(m);
@@ -700,6 +720,7 @@ rd_status_t rd_model_destroy(rd_model_t m) {
   if (m->dL32) cudaFree(m->dL32);
   if (m->dD64) cudaFree(m->dD64);
   if (m->dD32) cudaFree(m->dD32);
+  if (m->dPrism) cudaFree(m->dPrism);
   if (m->ws) cudaFree(m->ws);
   for (int k = 0; k < 2; ++k) {
     if (m->hbuf[k]) cudaFree(m->hbuf[k]);

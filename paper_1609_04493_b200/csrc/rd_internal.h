@@ -23,11 +23,14 @@ struct LinkConst {
   T alpha, beta;
 };
 
-// Per-link constants of the all-revolute thread kernel in Denavit-Hartenberg
-// (modified, Craig) frames: f_{i-1,i}(q) =
-// Rx(alpha) Tx(a) Rz(q + th0) Tz(d), i.e. R = Rx(alpha) Rz(q + th0),
-// p = (a, -sin(alpha) d, cos(alpha) d) = (p0, p1, p2); S_i = (0, e_z);
-// inertia as in LinkConst.
+// Per-link constants of the DH-frame kernels (thread, reverse, ABA-DH) in
+// Denavit-Hartenberg (modified, Craig) frames:
+// f_{i-1,i}(q) = Rx(alpha) Tx(a) Rz(theta) Tz(d), R = Rx(alpha) Rz(theta),
+// p = (a, -sin(alpha) d, cos(alpha) d) = (p0, p1, p2).  Revolute joint:
+// theta = th0 + q, d constant, S_i = (0, e_z).  Prismatic joint (flagged in a
+// separate per-link mask so this struct keeps its 17 scalars -- one more costs
+// the thread kernel 1.5 %): theta = th0, d = d0 + q, i.e.
+// p = (p0, p1 - sa q, p2 + ca q), S_i = (e_z, 0).  Inertia as in LinkConst.
 template <typename T>
 struct LinkDH {
   T ca, sa;       // cos/sin alpha
@@ -64,10 +67,11 @@ enum Strategy { kAuto = 0, kThread = 1, kWarpScan = 2, kGeneric = 3 };
 // status array (device int32[B], nullptr = none): 0, or the 1-based link of the
 // failing pivot (Omega_i <= 0 in the ABI sweep, tip-most first; JSIIA: the first
 // non-positive Cholesky pivot).
+// prism_mask: bit i set = link i prismatic (DH kernels; n <= 32 here).
 template <typename T>
 cudaError_t launch_rnea_thread(int n, const LinkDH<T>* L_host, const Boundary<T>& bnd,
                                int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
-                               cudaStream_t st, int* launches, bool* supported);
+                               cudaStream_t st, int* launches, bool* supported, uint32_t prism_mask = 0);
 template <typename T>
 cudaError_t launch_rnea_generic(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                                 int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
@@ -95,10 +99,11 @@ template <typename T>
 cudaError_t launch_rnea_block(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                               int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
                               cudaStream_t st, int* launches, bool* supported);
+// prism: device uint8[n], 1 = prismatic link (nullptr: all revolute).
 template <typename T>
 cudaError_t launch_rnea_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd,
                             int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
-                            cudaStream_t st, int* launches);
+                            cudaStream_t st, int* launches, const unsigned char* prism = nullptr);
 template <typename T>
 cudaError_t launch_aba_dh(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd,
                           int64_t B, const T* q, const T* qd, const T* tau, T* qdd,

@@ -218,19 +218,23 @@ __device__ __forceinline__ void bwd_step(const Rot<T>& R, T p0, T p1, T p2, cons
 // f = (R, p), R = Rx(alpha) Rz(theta), p = (p0, p1, p2) constant (LinkDH).
 // out = Ad_{f^-1} in = (R^T (v + w x p), R^T w), R^T = Rz^T Rx^T.
 template <typename T>
-__device__ __forceinline__ void dh_ad_finv(const LinkDH<T>& C, T s, T c, const T* in, T* out) {
-  const T x0 = fma(in[4], C.p2, fma(-in[5], C.p1, in[0]));
-  const T x1 = fma(in[5], C.p0, fma(-in[3], C.p2, in[1]));
-  const T x2 = fma(in[3], C.p1, fma(-in[4], C.p0, in[2]));
+__device__ __forceinline__ void dh_ad_finv(T ca, T sa, T p0, T p1, T p2, T s, T c, const T* in, T* out) {
+  const T x0 = fma(in[4], p2, fma(-in[5], p1, in[0]));
+  const T x1 = fma(in[5], p0, fma(-in[3], p2, in[1]));
+  const T x2 = fma(in[3], p1, fma(-in[4], p0, in[2]));
   // Rx^T x = (x0, ca x1 + sa x2, -sa x1 + ca x2); then Rz^T y = (c y0 + s y1, -s y0 + c y1, y2)
-  const T y1 = fma(C.ca, x1, C.sa * x2), y2 = fma(C.ca, x2, -(C.sa * x1));
+  const T y1 = fma(ca, x1, sa * x2), y2 = fma(ca, x2, -(sa * x1));
   out[0] = fma(c, x0, s * y1);
   out[1] = fma(c, y1, -(s * x0));
   out[2] = y2;
-  const T u1 = fma(C.ca, in[4], C.sa * in[5]), u2 = fma(C.ca, in[5], -(C.sa * in[4]));
+  const T u1 = fma(ca, in[4], sa * in[5]), u2 = fma(ca, in[5], -(sa * in[4]));
   out[3] = fma(c, in[3], s * u1);
   out[4] = fma(c, u1, -(s * in[3]));
   out[5] = u2;
+}
+template <typename T>
+__device__ __forceinline__ void dh_ad_finv(const LinkDH<T>& C, T s, T c, const T* in, T* out) {
+  dh_ad_finv(C.ca, C.sa, C.p0, C.p1, C.p2, s, c, in, out);
 }
 
 // F = Fh + Ad^T_{f^-1} Fn = Fh + (R f, p x (R f) + R m), R = Rx(alpha) Rz(theta)
@@ -253,16 +257,20 @@ __device__ __forceinline__ void dh_bwd(T ca, T sa, T p0, T p1, T p2, T s, T c, c
 // out = Ad_f in = (R v + p x (R w), R w), R = Rx(alpha) Rz(theta): the inverse of
 // dh_ad_finv (used to re-derive V_{i-1}, Vdot_{i-1} from V_i, Vdot_i).
 template <typename T>
-__device__ __forceinline__ void dh_ad_f(const LinkDH<T>& C, T s, T c, const T* in, T* out) {
+__device__ __forceinline__ void dh_ad_f(T ca, T sa, T p0, T p1, T p2, T s, T c, const T* in, T* out) {
   // Rz y = (c y0 - s y1, s y0 + c y1, y2); Rx z = (z0, ca z1 - sa z2, sa z1 + ca z2)
   const T a0 = fma(c, in[3], -(s * in[4])), a1 = fma(s, in[3], c * in[4]), a2 = in[5];
-  const T w0 = a0, w1 = fma(C.ca, a1, -(C.sa * a2)), w2 = fma(C.sa, a1, C.ca * a2);
+  const T w0 = a0, w1 = fma(ca, a1, -(sa * a2)), w2 = fma(sa, a1, ca * a2);
   const T b0 = fma(c, in[0], -(s * in[1])), b1 = fma(s, in[0], c * in[1]), b2 = in[2];
-  const T v0 = b0, v1 = fma(C.ca, b1, -(C.sa * b2)), v2 = fma(C.sa, b1, C.ca * b2);
-  out[0] = fma(C.p1, w2, fma(-C.p2, w1, v0));
-  out[1] = fma(C.p2, w0, fma(-C.p0, w2, v1));
-  out[2] = fma(C.p0, w1, fma(-C.p1, w0, v2));
+  const T v0 = b0, v1 = fma(ca, b1, -(sa * b2)), v2 = fma(sa, b1, ca * b2);
+  out[0] = fma(p1, w2, fma(-p2, w1, v0));
+  out[1] = fma(p2, w0, fma(-p0, w2, v1));
+  out[2] = fma(p0, w1, fma(-p1, w0, v2));
   out[3] = w0; out[4] = w1; out[5] = w2;
+}
+template <typename T>
+__device__ __forceinline__ void dh_ad_f(const LinkDH<T>& C, T s, T c, const T* in, T* out) {
+  dh_ad_f(C.ca, C.sa, C.p0, C.p1, C.p2, s, c, in, out);
 }
 
 }  // namespace rd

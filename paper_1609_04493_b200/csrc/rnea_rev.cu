@@ -31,15 +31,36 @@ constexpr int kRevThreads = 128;
 #endif
 constexpr int kRevPD = RD_REV_PD, kRevU = RD_REV_U;
 
-template <typename T>
+// (sin, cos) of theta and the variable translation of link C: revolute theta =
+// th0 + q; prismatic (PR && prism) theta = th0, p = (p0, p1 - sa q, p2 + ca q).
+template <bool PR, typename T>
+__device__ __forceinline__ void dh_link(const LinkDH<T>& C, bool prism, T qi, T* s, T* c, T* p1, T* p2) {
+  const T qa = (PR && prism) ? T(0) : qi;
+  if (sizeof(T) == 8) {
+    rd_sincos(qa + C.th0, s, c);
+  } else {
+    T s0, c0;
+    rd_sincos(qa, &s0, &c0);
+    *s = fma(s0, C.cth0, c0 * C.sth0);
+    *c = fma(c0, C.cth0, -(s0 * C.sth0));
+  }
+  const T dq = (PR && prism) ? qi : T(0);
+  *p1 = PR ? fma(-C.sa, dq, C.p1) : C.p1;
+  *p2 = PR ? fma(C.ca, dq, C.p2) : C.p2;
+}
+
+template <typename T, bool PR>
 __global__ void __launch_bounds__(kRevThreads, 4)
 rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
                 const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
-                T* __restrict__ tau) {
+                T* __restrict__ tau, const unsigned char* __restrict__ prism_g) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LinkDH<T>* L = reinterpret_cast<LinkDH<T>*>(smem_raw);       // model constants, broadcast reads
+  unsigned char* PRs = smem_raw + (size_t)n * sizeof(LinkDH<T>);   // prismatic flags (PR only)
   for (int i = threadIdx.x; i < n * (int)(sizeof(LinkDH<T>) / sizeof(T)); i += blockDim.x)
     reinterpret_cast<T*>(L)[i] = reinterpret_cast<const T*>(Lg)[i];
+  if (PR)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) PRs[i] = prism_g[i];
   __syncthreads();
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
     const T* pq = q + b;
@@ -66,24 +87,21 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
         aq[PD - 1] = __ldg(pq + o); aqd[PD - 1] = __ldg(pqd + o); aqa[PD - 1] = __ldg(pqa + o);
       }
       const LinkDH<T> C = L[i];
-      T s, c;
-      if (sizeof(T) == 8) {
-        rd_sincos(qi + C.th0, &s, &c);
-      } else {
-        T s0, c0;
-        rd_sincos(qi, &s0, &c0);
-        s = fma(s0, C.cth0, c0 * C.sth0);
-        c = fma(c0, C.cth0, -(s0 * C.sth0));
-      }
+      const bool pz = PR && PRs[i];
+      T s, c, lp1, lp2;
+      dh_link<PR>(C, pz, qi, &s, &c, &lp1, &lp2);
       T Vn[6], Vdn[6];
-      dh_ad_finv(C, s, c, V, Vn);
-      dh_ad_finv(C, s, c, Vd, Vdn);
-      Vn[5] += qdi;
-      Vdn[5] += qai;
-      Vdn[0] = fma(qdi, Vn[1], Vdn[0]);
-      Vdn[1] = fma(-qdi, Vn[0], Vdn[1]);
-      Vdn[3] = fma(qdi, Vn[4], Vdn[3]);
-      Vdn[4] = fma(-qdi, Vn[3], Vdn[4]);
+      dh_ad_finv(C.ca, C.sa, C.p0, lp1, lp2, s, c, V, Vn);
+      dh_ad_finv(C.ca, C.sa, C.p0, lp1, lp2, s, c, Vd, Vdn);
+      // S qd = (sp e_z, sr e_z); ad_V(S qd) = (sp w x e_z + sr v x e_z, sr w x e_z)
+      const T sr = pz ? T(0) : qdi, sp = pz ? qdi : T(0), ar = pz ? T(0) : qai, ap = pz ? qai : T(0);
+      Vn[5] += sr;
+      Vdn[5] += ar;
+      if (PR) { Vn[2] += sp; Vdn[2] += ap; }
+      Vdn[0] = fma(sr, Vn[1], PR ? fma(sp, Vn[4], Vdn[0]) : Vdn[0]);
+      Vdn[1] = fma(-sr, Vn[0], PR ? fma(-sp, Vn[3], Vdn[1]) : Vdn[1]);
+      Vdn[3] = fma(sr, Vn[4], Vdn[3]);
+      Vdn[4] = fma(-sr, Vn[3], Vdn[4]);
 #pragma unroll
       for (int k = 0; k < 6; ++k) { V[k] = Vn[k]; Vd[k] = Vdn[k]; }
     }
@@ -109,60 +127,65 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
       }
       if (i < n - 1) tau[(int64_t)(i + 1) * B + b] = tp;
       const LinkDH<T> C = L[i];
+      const bool pz = PR && PRs[i];
       T Fh[6], Fo[6];
       bias_force(C, V, Vd, Fh);
       dh_bwd(ca, sa, p0, p1, p2, sn, cn, F, Fh, Fo);
 #pragma unroll
       for (int k = 0; k < 6; ++k) F[k] = Fo[k];
-      tp = F[5];
-      T s, c;
-      if (sizeof(T) == 8) {
-        rd_sincos(qi + C.th0, &s, &c);
-      } else {
-        T s0, c0;
-        rd_sincos(qi, &s0, &c0);
-        s = fma(s0, C.cth0, c0 * C.sth0);
-        c = fma(c0, C.cth0, -(s0 * C.sth0));
-      }
+      tp = pz ? F[2] : F[5];                        // tau_i = S_i^T F_i
+      T s, c, lp1, lp2;
+      dh_link<PR>(C, pz, qi, &s, &c, &lp1, &lp2);
       // V_{i-1}, Vdot_{i-1}
+      const T sr = pz ? T(0) : qdi, sp = pz ? qdi : T(0), ar = pz ? T(0) : qai, ap = pz ? qai : T(0);
       T x[6], y[6];
 #pragma unroll
       for (int k = 0; k < 6; ++k) { x[k] = V[k]; y[k] = Vd[k]; }
-      x[5] -= qdi;
-      y[5] -= qai;
-      y[0] = fma(-qdi, V[1], y[0]);
-      y[1] = fma(qdi, V[0], y[1]);
-      y[3] = fma(-qdi, V[4], y[3]);
-      y[4] = fma(qdi, V[3], y[4]);
-      dh_ad_f(C, s, c, x, V);
-      dh_ad_f(C, s, c, y, Vd);
-      ca = C.ca; sa = C.sa; p0 = C.p0; p1 = C.p1; p2 = C.p2; sn = s; cn = c;
+      x[5] -= sr;
+      y[5] -= ar;
+      if (PR) { x[2] -= sp; y[2] -= ap; }
+      y[0] = fma(-sr, V[1], PR ? fma(-sp, V[4], y[0]) : y[0]);
+      y[1] = fma(sr, V[0], PR ? fma(sp, V[3], y[1]) : y[1]);
+      y[3] = fma(-sr, V[4], y[3]);
+      y[4] = fma(sr, V[3], y[4]);
+      dh_ad_f(C.ca, C.sa, C.p0, lp1, lp2, s, c, x, V);
+      dh_ad_f(C.ca, C.sa, C.p0, lp1, lp2, s, c, y, Vd);
+      ca = C.ca; sa = C.sa; p0 = C.p0; p1 = lp1; p2 = lp2; sn = s; cn = c;
     }
     tau[b] = tp;
   }
 }
 
-template <typename T>
-cudaError_t launch_rnea_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
-                            const T* qd, const T* qdd, T* tau, cudaStream_t st, int* launches) {
-  const size_t smem = (size_t)n * sizeof(LinkDH<T>);
+template <typename T, bool PR>
+static cudaError_t launch_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
+                              const T* qd, const T* qdd, T* tau, cudaStream_t st, const unsigned char* prism) {
+  const size_t smem = (size_t)n * sizeof(LinkDH<T>) + (PR ? (size_t)n : 0);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(rnea_rev_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(rnea_rev_kernel<T, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
   int64_t grid = (B + kRevThreads - 1) / kRevThreads;
   const int64_t cap = (int64_t)num_sms() * 4;
   if (grid > cap) grid = cap;
-  rnea_rev_kernel<T><<<(unsigned)grid, kRevThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau);
-  ++*launches;
+  rnea_rev_kernel<T, PR><<<(unsigned)grid, kRevThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau, prism);
   return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_rnea_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
+                            const T* qd, const T* qdd, T* tau, cudaStream_t st, int* launches,
+                            const unsigned char* prism) {
+  ++*launches;
+  return prism ? launch_rev<T, true>(n, L_dev, bnd, B, q, qd, qdd, tau, st, prism)
+               : launch_rev<T, false>(n, L_dev, bnd, B, q, qd, qdd, tau, st, nullptr);
 }
 
 template cudaError_t launch_rnea_rev<double>(int, const LinkDH<double>*, const Boundary<double>&, int64_t,
                                              const double*, const double*, const double*, double*, cudaStream_t,
-                                             int*);
+                                             int*, const unsigned char*);
 template cudaError_t launch_rnea_rev<float>(int, const LinkDH<float>*, const Boundary<float>&, int64_t,
-                                            const float*, const float*, const float*, float*, cudaStream_t, int*);
+                                            const float*, const float*, const float*, float*, cudaStream_t, int*,
+                                            const unsigned char*);
 
 }  // namespace rd

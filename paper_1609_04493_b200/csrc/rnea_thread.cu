@@ -32,6 +32,7 @@ struct ThreadParams {
   Boundary<T> bnd;
   int n;          // links
   int lt;         // links stashed in TMEM (the rest in shared memory)
+  uint32_t prism; // bit k: link k is prismatic (PR instantiation only)
 };
 
 // ------------------------------------------------------------------ TMEM helpers
@@ -204,7 +205,7 @@ __device__ __forceinline__ void bwd_init(BwdState<T>& g, const ThreadParams<T>& 
   g.ca = 1; g.sa = 0; g.p0 = g.p1 = g.p2 = 0; g.s = 0; g.c = 1;   // f_{n,n+1} = I (A5)
 }
 // forward link k: V_k, Vdot_k, Fhat_k -> st[8]
-template <typename T, int PD>
+template <bool PR, typename T, int PD>
 __device__ __forceinline__ void fwd_link(FwdState<T, PD>& f, const ThreadParams<T>& P, int64_t B, int k, T* st) {
   const int n = P.n;
   // this link's inputs (loaded two links earlier) and the loads for link k+2
@@ -219,26 +220,49 @@ __device__ __forceinline__ void fwd_link(FwdState<T, PD>& f, const ThreadParams<
   const T f_qd = __ldg((here ? f.pqd : f.xqd) + off2);
   const T f_qa = __ldg((here ? f.pqa : f.xqa) + off2);
   const LinkDH<T>& C = P.L[k];
+  // PR (the model has prismatic joints): link type from C.pr (warp-uniform), selects only.
+  const bool prism = PR && ((P.prism >> k) & 1u);
+  const T qang = prism ? T(0) : cq;               // revolute: theta = th0 + q; prismatic: th0
   T s, c;
   if (sizeof(T) == 8) {
-    rd_sincos(cq + C.th0, &s, &c);            // fp64: rounding of q + th0 is ~ulp(q)
+    rd_sincos(qang + C.th0, &s, &c);          // fp64: rounding of q + th0 is ~ulp(q)
   } else {
     T s0, c0;                                     // fp32: sin/cos(q) then add th0 exactly
-    rd_sincos(cq, &s0, &c0);
+    rd_sincos(qang, &s0, &c0);
     s = fma(s0, C.cth0, c0 * C.sth0);
     c = fma(c0, C.cth0, -(s0 * C.sth0));
   }
-  // Eq. (1): V = Ad_{f^-1} V + S qd, Vd = Ad_{f^-1} Vd + S qdd + ad_V(S qd), S = (0, e_z)
+  // Eq. (1): V = Ad_{f^-1} V + S qd, Vd = Ad_{f^-1} Vd + S qdd + ad_V(S qd),
+  // S = (0, e_z) (revolute) or (e_z, 0) (prismatic, d = d0 + q)
   T Vn[6], Vdn[6];
-  dh_ad_finv(C, s, c, f.V, Vn);
-  dh_ad_finv(C, s, c, f.Vd, Vdn);
-  Vn[5] += cqd;
-  Vdn[5] += cqa;
-  Vdn[0] = fma(cqd, Vn[1], Vdn[0]);
-  Vdn[1] = fma(-cqd, Vn[0], Vdn[1]);
-  Vdn[3] = fma(cqd, Vn[4], Vdn[3]);
-  Vdn[4] = fma(-cqd, Vn[3], Vdn[4]);
-  st[0] = s;
+  if (PR) {
+    const T dq = prism ? cq : T(0);
+    const T p1 = fma(-C.sa, dq, C.p1), p2 = fma(C.ca, dq, C.p2);
+    dh_ad_finv(C.ca, C.sa, C.p0, p1, p2, s, c, f.V, Vn);
+    dh_ad_finv(C.ca, C.sa, C.p0, p1, p2, s, c, f.Vd, Vdn);
+    const T sr = prism ? T(0) : cqd, sp = prism ? cqd : T(0);
+    const T ar = prism ? T(0) : cqa, ap = prism ? cqa : T(0);
+    Vn[5] += sr;
+    Vn[2] += sp;
+    Vdn[5] += ar;
+    Vdn[2] += ap;
+    // ad_V (sp e_z, sr e_z) = (sp w x e_z + sr v x e_z, sr w x e_z)
+    Vdn[0] = fma(sr, Vn[1], fma(sp, Vn[4], Vdn[0]));
+    Vdn[1] = fma(-sr, Vn[0], fma(-sp, Vn[3], Vdn[1]));
+    Vdn[3] = fma(sr, Vn[4], Vdn[3]);
+    Vdn[4] = fma(-sr, Vn[3], Vdn[4]);
+    st[0] = prism ? cq : s;                         // prismatic: (s, c) are constants, keep q
+  } else {
+    dh_ad_finv(C, s, c, f.V, Vn);
+    dh_ad_finv(C, s, c, f.Vd, Vdn);
+    Vn[5] += cqd;
+    Vdn[5] += cqa;
+    Vdn[0] = fma(cqd, Vn[1], Vdn[0]);
+    Vdn[1] = fma(-cqd, Vn[0], Vdn[1]);
+    Vdn[3] = fma(cqd, Vn[4], Vdn[3]);
+    Vdn[4] = fma(-cqd, Vn[3], Vdn[4]);
+    st[0] = s;
+  }
   st[1] = c;
   bias_force(C, Vn, Vdn, st + 2);
 #pragma unroll
@@ -248,7 +272,7 @@ __device__ __forceinline__ void fwd_link(FwdState<T, PD>& f, const ThreadParams<
   f.a_q[kPD - 1] = f_q; f.a_qd[kPD - 1] = f_qd; f.a_qa[kPD - 1] = f_qa;
 }
 // backward link i from its stash cur[8]: F_i, tau_i, then (R, p) of link i for link i-1
-template <typename T>
+template <bool PR, typename T>
 __device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& P, int64_t B, int i,
                                          const T* cur, T* __restrict__ tau) {
   T Fo[6];
@@ -260,18 +284,29 @@ __device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& 
   dh_bwd(g.ca, g.sa, g.p0, g.p1, g.p2, g.s, g.c, g.F, cur + 2, Fo);
 #pragma unroll
   for (int j = 0; j < 6; ++j) g.F[j] = Fo[j];
+  const LinkDH<T>& C = P.L[i];
+  const bool prism = PR && ((P.prism >> i) & 1u);
+  const T ti = prism ? g.F[2] : g.F[5];            // tau_i = S_i^T F_i
 #if RD_TAU_DEFER
-  g.tp = g.F[5];
+  g.tp = ti;
   g.ip = i;
 #else
-  if (g.valid) tau[(int64_t)i * B + g.b] = g.F[5];
+  if (g.valid) tau[(int64_t)i * B + g.b] = ti;
 #endif
-  const LinkDH<T>& C = P.L[i];
-  g.ca = C.ca; g.sa = C.sa; g.p0 = C.p0; g.p1 = C.p1; g.p2 = C.p2;
-  g.s = cur[0]; g.c = cur[1];
+  g.ca = C.ca; g.sa = C.sa; g.p0 = C.p0;
+  if (PR) {
+    const T dq = prism ? cur[0] : T(0);
+    g.p1 = fma(-C.sa, dq, C.p1);
+    g.p2 = fma(C.ca, dq, C.p2);
+    g.s = prism ? C.sth0 : cur[0];
+  } else {
+    g.p1 = C.p1; g.p2 = C.p2;
+    g.s = cur[0];
+  }
+  g.c = cur[1];
 }
 
-template <typename T, int W>
+template <typename T, int W, bool PR>
 __global__ void __launch_bounds__(W * 32, 1)
 rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
                       const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
@@ -337,7 +372,7 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
       for (int i = n - 1; i >= 0; --i) {
         T cur[8];
         get_any(bpar ? n - 1 - i : i, cur);
-        bwd_link(g, P, B, i, cur, tau);
+        bwd_link<PR>(g, P, B, i, cur, tau);
       }
       bwd_flush(g, B, tau);
       break;
@@ -348,7 +383,7 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
       // prologue: forward of the first tile alone (parity 0: slot = link)
       for (int k = 0; k < n; ++k) {
         T st[8];
-        fwd_link(f, P, B, k, st);
+        fwd_link<PR>(f, P, B, k, st);
         put_any(k, st);
       }
     } else {
@@ -360,8 +395,8 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
         const int slot = bpar ? k : n - 1 - k;
         T cur[8], st[8];
         get_smem(slot, cur);
-        bwd_link(g, P, B, n - 1 - k, cur, tau);
-        fwd_link(f, P, B, k, st);
+        bwd_link<PR>(g, P, B, n - 1 - k, cur, tau);
+        fwd_link<PR>(f, P, B, k, st);
         put_smem(slot, st);
       };
       auto tmem_seg = [&](int k0, int k1) {
@@ -377,8 +412,8 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
           T cur[8], st[8];
           TmemIO<T>::unpack(r, cur);
           TmemIO<T>::ld(tbase + (uint32_t)(slot_nx * KC), r);       // next step's slot, in flight
-          bwd_link(g, P, B, n - 1 - k, cur, tau);
-          fwd_link(f, P, B, k, st);
+          bwd_link<PR>(g, P, B, n - 1 - k, cur, tau);
+          fwd_link<PR>(f, P, B, k, st);
           TmemIO<T>::st(tbase + (uint32_t)(slot * KC), st);
         }
         TmemIO<T>::wait(r);
@@ -443,28 +478,28 @@ bool thread_kernel_has_n(int n, bool fp64) {
   return fp64 ? plan_for<double>(n, &p) : plan_for<float>(n, &p);
 }
 
-template <typename T, int W>
+template <typename T, int W, bool PR>
 static cudaError_t launch_w(const ThreadParams<T>& P, size_t smem, int64_t B, const T* q, const T* qd,
                             const T* qdd, T* tau, cudaStream_t st) {
   static thread_local int attr_dev = -1;          // the opt-in is per device; set it once
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(rnea_thread_pp_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(rnea_thread_pp_kernel<T, W, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(kSmemCap - 1024));
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
   const int64_t ntiles = (B + W * 32 - 1) / (W * 32);
   const int64_t grid = ntiles < num_sms() ? ntiles : num_sms();
-  rnea_thread_pp_kernel<T, W><<<(unsigned)grid, W * 32, smem, st>>>(P, B, q, qd, qdd, tau);
+  rnea_thread_pp_kernel<T, W, PR><<<(unsigned)grid, W * 32, smem, st>>>(P, B, q, qd, qdd, tau);
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_rnea_thread(int n, const LinkDH<T>* L_host, const Boundary<T>& bnd, int64_t B,
                                const T* q, const T* qd, const T* qdd, T* tau, cudaStream_t st,
-                               int* launches, bool* supported) {
+                               int* launches, bool* supported, uint32_t prism_mask) {
   StashPlan plan;
   *supported = n >= 1 && n <= kMaxThreadN && plan_for<T>(n, &plan);
   if (!*supported) return cudaSuccess;
@@ -474,15 +509,20 @@ cudaError_t launch_rnea_thread(int n, const LinkDH<T>* L_host, const Boundary<T>
   P.n = n;
   P.lt = plan.lt;
   ++*launches;
-  if (plan.W == 16) return launch_w<T, 16>(P, plan.smem, B, q, qd, qdd, tau, st);
-  return launch_w<T, 8>(P, plan.smem, B, q, qd, qdd, tau, st);
+  P.prism = prism_mask;
+  if (prism_mask != 0) {                           // any prismatic joint: the PR instantiation
+    if (plan.W == 16) return launch_w<T, 16, true>(P, plan.smem, B, q, qd, qdd, tau, st);
+    return launch_w<T, 8, true>(P, plan.smem, B, q, qd, qdd, tau, st);
+  }
+  if (plan.W == 16) return launch_w<T, 16, false>(P, plan.smem, B, q, qd, qdd, tau, st);
+  return launch_w<T, 8, false>(P, plan.smem, B, q, qd, qdd, tau, st);
 }
 
 template cudaError_t launch_rnea_thread<double>(int, const LinkDH<double>*, const Boundary<double>&, int64_t,
                                                 const double*, const double*, const double*, double*,
-                                                cudaStream_t, int*, bool*);
+                                                cudaStream_t, int*, bool*, uint32_t);
 template cudaError_t launch_rnea_thread<float>(int, const LinkDH<float>*, const Boundary<float>&, int64_t,
                                                const float*, const float*, const float*, float*,
-                                               cudaStream_t, int*, bool*);
+                                               cudaStream_t, int*, bool*, uint32_t);
 
 }  // namespace rd

@@ -152,6 +152,20 @@ def test_prismatic_and_screw_joints_generic(rd, dtype):
         check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype, strategy=strat)
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("n,pf", [(1, 1.0), (2, 0.5), (7, 0.4), (30, 0.3), (31, 0.3), (100, 0.3)])
+def test_prismatic_joints_dh_kernels(rd, n, pf, dtype):
+    # revolute + prismatic chains run the DH-frame kernels (prismatic: d = d0 + q)
+    r = synth.random_chain(n, 880 + n, prismatic_fraction=pf)
+    q, qd, qdd = synth.states(14, n, 0, 1500)
+    model = rd.Model.from_robot(r, synth.GRAVITY_Z)
+    model.set_strategy("thread")
+    want = "thread" if (n <= 30 or (n <= 32 and dtype == torch.float32)) else "reverse"
+    assert model.resolve_strategy(1500, dtype == torch.float64) == want
+    for strat in ("thread", "reverse"):
+        check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype, strategy=strat)
+
+
 def test_pendulum_closed_form_on_gpu(rd):
     m, l, Izz, g = 1.7, 0.8, 0.05, 9.81
     model = rd.Model.from_robot(synth.pendulum(m, l, Izz), (0, -g, 0))
