@@ -189,19 +189,25 @@ aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int
 }
 
 // ---------------------------------------------------------------- DH-frame variant
-// All-revolute chains in DH frames (the THREAD ID kernel's frames): same three
-// sweeps, with the plane-rotation congruence (dh_congruence) and the 22-flop
-// Ad maps; S = (0, e_z) so U = Jhat[:, 5], D = U[5], u = tau - phat[5].
-template <typename T, int MB>
+// Revolute / prismatic chains in DH frames (the THREAD ID kernel's frames): same
+// three sweeps, with the plane-rotation congruence (dh_congruence) and the
+// 22-flop Ad maps.  Revolute S = (0, e_z): U = Jhat[:, 5], D = U[5],
+// u = tau - phat[5]; prismatic (PR instantiation, per-link flag) S = (e_z, 0):
+// U = Jhat[:, 2], D = U[2], u = tau - phat[2], d = d0 + q.
+template <typename T, int MB, bool PR>
 __global__ void __launch_bounds__(kAbaThreads, MB)
 aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
               const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ tau_in,
-              T* __restrict__ qdd_out, T* __restrict__ ws, int64_t slots, int32_t* __restrict__ status) {
+              T* __restrict__ qdd_out, T* __restrict__ ws, int64_t slots, int32_t* __restrict__ status,
+              const unsigned char* __restrict__ prism_g) {
   // model constants staged in shared memory (broadcast reads, no long-scoreboard waits)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LinkDH<T>* L = reinterpret_cast<LinkDH<T>*>(smem_raw);
+  unsigned char* PRs = smem_raw + (size_t)n * sizeof(LinkDH<T>);   // prismatic flags (PR only)
   for (int i = threadIdx.x; i < n * (int)(sizeof(LinkDH<T>) / sizeof(T)); i += blockDim.x)
     reinterpret_cast<T*>(L)[i] = reinterpret_cast<const T*>(Lg)[i];
+  if (PR)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) PRs[i] = prism_g[i];
   __syncthreads();
   const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= slots) return;
@@ -231,11 +237,20 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
           aq[kS1PD - 1] = __ldg(pq + o); aqd[kS1PD - 1] = __ldg(pqd + o);
         }
         const LinkDH<T>& C = L[i];
-        T s, c;
-        dh_sincos(C, cq, &s, &c);
         T Vn[6];
-        dh_ad_finv(C, s, c, V, Vn);
-        Vn[5] += cqd;
+        if constexpr (PR) {
+          const bool pz = PRs[i];
+          T s, c, lp1, lp2;
+          dh_link<PR>(C, pz, cq, &s, &c, &lp1, &lp2);
+          dh_ad_finv(C.ca, C.sa, C.p0, lp1, lp2, s, c, V, Vn);
+          Vn[5] += pz ? T(0) : cqd;
+          Vn[2] += pz ? cqd : T(0);
+        } else {
+          T s, c;
+          dh_sincos(C, cq, &s, &c);
+          dh_ad_finv(C, s, c, V, Vn);
+          Vn[5] += cqd;
+        }
 #pragma unroll
         for (int k = 0; k < 6; ++k) V[k] = Vn[k];
       }
@@ -254,10 +269,21 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
       const int64_t o = (int64_t)max(i - 1, 0) * B;
       const T nq = __ldg(pq + o), nqd = __ldg(pqd + o), nt = __ldg(pt + o);
       const LinkDH<T>& C = L[i];
-      T s, c;
-      dh_sincos(C, cq, &s, &c);
+      const bool pz = PR && PRs[i];
+      T s, c, lp1, lp2;
       const T qdi = cqd;
-      T cc[6] = {qdi * V[1], -qdi * V[0], 0, qdi * V[4], -qdi * V[3], 0};   // ad_V(e_z qd)
+      T cc[6];
+      if constexpr (PR) {
+        dh_link<PR>(C, pz, cq, &s, &c, &lp1, &lp2);
+        // c_i = ad_V(S qd), S qd = (sp e_z, sr e_z)
+        const T sr = pz ? T(0) : qdi, sp = pz ? qdi : T(0);
+        cc[0] = fma(sp, V[4], sr * V[1]); cc[1] = -fma(sp, V[3], sr * V[0]); cc[2] = 0;
+        cc[3] = sr * V[4]; cc[4] = -sr * V[3]; cc[5] = 0;
+      } else {
+        dh_sincos(C, cq, &s, &c);
+        lp1 = C.p1; lp2 = C.p2;
+        cc[0] = qdi * V[1]; cc[1] = -qdi * V[0]; cc[2] = 0; cc[3] = qdi * V[4]; cc[4] = -qdi * V[3]; cc[5] = 0;
+      }
       T ph[6];
       bias_force(C, V, zero6, ph);
       dh_inertia(C, K);
@@ -265,12 +291,16 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
       for (int k = 0; k < 6; ++k) { K.a[k] += Kc.a[k]; K.c[k] += Kc.c[k]; ph[k] += pc[k]; }
 #pragma unroll
       for (int k = 0; k < 9; ++k) K.b[k] += Kc.b[k];
-      // U = K e_5 = (B[:, 2], C[:, 2])
+      // revolute: U = K e_5 = (B[:, 2], C[:, 2]); prismatic: U = K e_2 = (A[:, 2], B[2, :])
       T U[6] = {K.b[2], K.b[5], K.b[8], K.c[4], K.c[5], K.c[2]};
-      const T D = U[5];
+      if (PR && pz) {
+        U[0] = K.a[4]; U[1] = K.a[5]; U[2] = K.a[2];
+        U[3] = K.b[6]; U[4] = K.b[7]; U[5] = K.b[8];
+      }
+      const T D = (PR && pz) ? U[2] : U[5];
       const T invD = (D > (T)0) ? (T)1 / D : (T)NAN;
       if (!(D > (T)0) && fail == 0) fail = i + 1;
-      const T ub = (ct - ph[5]) * invD;
+      const T ub = (ct - ((PR && pz) ? ph[2] : ph[5])) * invD;
       T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
 #pragma unroll
       for (int k = 0; k < 6; ++k) w[k * slots] = U[k] * invD;
@@ -282,13 +312,24 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
 #pragma unroll
         for (int k = 0; k < 6; ++k) pa[k] = ph[k] + Kcc[k] + U[k] * ub;
         Kc = K;
-        dh_congruence(C, s, c, Kc);
-        dh_bwd(C.ca, C.sa, C.p0, C.p1, C.p2, s, c, pa, zero6, pc);
+        if constexpr (PR) {
+          dh_congruence(C.ca, C.sa, C.p0, lp1, lp2, s, c, Kc);
+          dh_bwd(C.ca, C.sa, C.p0, lp1, lp2, s, c, pa, zero6, pc);
+        } else {
+          dh_congruence(C, s, c, Kc);
+          dh_bwd(C.ca, C.sa, C.p0, C.p1, C.p2, s, c, pa, zero6, pc);
+        }
         T x[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) x[k] = V[k];
-        x[5] -= qdi;
-        dh_ad_f(C, s, c, x, V);                    // V_{i-1} = Ad_{f_i}(V_i - S qd)
+        if constexpr (PR) {
+          x[5] -= pz ? T(0) : qdi;
+          x[2] -= pz ? qdi : T(0);
+          dh_ad_f(C.ca, C.sa, C.p0, lp1, lp2, s, c, x, V);   // V_{i-1} = Ad_{f_i}(V_i - S qd)
+        } else {
+          x[5] -= qdi;
+          dh_ad_f(C, s, c, x, V);
+        }
       }
       cq = nq; cqd = nqd; ct = nt;
     }
@@ -345,23 +386,39 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
         for (int k = 0; k < 6; ++k) Ub[k] = w[k * slots];
         const T ub = w[6 * slots];
 #endif
-        T s, c;
-        dh_sincos(C, cq3, &s, &c);
+        const bool pz = PR && PRs[i];
         const T qdi = cqd3;
         T Vn[6], an[6];
-        dh_ad_finv(C, s, c, V, Vn);
-        Vn[5] += qdi;
-        dh_ad_finv(C, s, c, a, an);
-        an[0] = fma(qdi, Vn[1], an[0]);
-        an[1] = fma(-qdi, Vn[0], an[1]);
-        an[3] = fma(qdi, Vn[4], an[3]);
-        an[4] = fma(-qdi, Vn[3], an[4]);
+        if constexpr (PR) {
+          T s, c, lp1, lp2;
+          dh_link<PR>(C, pz, cq3, &s, &c, &lp1, &lp2);
+          const T sr = pz ? T(0) : qdi, sp = pz ? qdi : T(0);
+          dh_ad_finv(C.ca, C.sa, C.p0, lp1, lp2, s, c, V, Vn);
+          Vn[5] += sr;
+          Vn[2] += sp;
+          dh_ad_finv(C.ca, C.sa, C.p0, lp1, lp2, s, c, a, an);
+          an[0] = fma(sr, Vn[1], fma(sp, Vn[4], an[0]));
+          an[1] = fma(-sr, Vn[0], fma(-sp, Vn[3], an[1]));
+          an[3] = fma(sr, Vn[4], an[3]);
+          an[4] = fma(-sr, Vn[3], an[4]);
+        } else {
+          T s, c;
+          dh_sincos(C, cq3, &s, &c);
+          dh_ad_finv(C, s, c, V, Vn);
+          Vn[5] += qdi;
+          dh_ad_finv(C, s, c, a, an);
+          an[0] = fma(qdi, Vn[1], an[0]);
+          an[1] = fma(-qdi, Vn[0], an[1]);
+          an[3] = fma(qdi, Vn[4], an[3]);
+          an[4] = fma(-qdi, Vn[3], an[4]);
+        }
         T Ua = 0;
 #pragma unroll
         for (int k = 0; k < 6; ++k) Ua = fma(Ub[k], an[k], Ua);
         const T qddi = ub - Ua;
         qdd_out[(int64_t)i * B + b] = qddi;
-        an[5] += qddi;
+        if (PR && pz) an[2] += qddi;
+        else an[5] += qddi;
 #pragma unroll
         for (int k = 0; k < 6; ++k) { a[k] = an[k]; V[k] = Vn[k]; }
       }
@@ -369,26 +426,36 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
   }
 }
 
+template <typename T, bool PR>
+static cudaError_t launch_aba_dh_pr(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B,
+                                    const T* q, const T* qd, const T* tau, T* qdd, T* ws, int64_t ws_slots,
+                                    cudaStream_t st, int32_t* status, const unsigned char* prism) {
+  const int64_t grid = (ws_slots + kAbaThreads - 1) / kAbaThreads;
+  const size_t smem = (size_t)n * sizeof(LinkDH<T>) + (PR ? (size_t)n : 0);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(aba_dh_kernel<T, 3, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  aba_dh_kernel<T, 3, PR><<<(unsigned)grid, kAbaThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws,
+                                                                      ws_slots, status, prism);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_aba_dh(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                           const T* qd, const T* tau, T* qdd, T* ws, int64_t ws_slots, cudaStream_t st,
-                          int* launches, int32_t* status) {
-  const int64_t grid = (ws_slots + kAbaThreads - 1) / kAbaThreads;
-  const size_t smem = (size_t)n * sizeof(LinkDH<T>);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(aba_dh_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  aba_dh_kernel<T, 3><<<(unsigned)grid, kAbaThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots, status);
+                          int* launches, int32_t* status, const unsigned char* prism) {
   ++*launches;
-  return cudaGetLastError();
+  return prism ? launch_aba_dh_pr<T, true>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots, st, status, prism)
+               : launch_aba_dh_pr<T, false>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots, st, status, nullptr);
 }
 template cudaError_t launch_aba_dh<double>(int, const LinkDH<double>*, const Boundary<double>&, int64_t,
                                            const double*, const double*, const double*, double*, double*, int64_t,
-                                           cudaStream_t, int*, int32_t*);
+                                           cudaStream_t, int*, int32_t*, const unsigned char*);
 template cudaError_t launch_aba_dh<float>(int, const LinkDH<float>*, const Boundary<float>&, int64_t,
                                           const float*, const float*, const float*, float*, float*, int64_t,
-                                          cudaStream_t, int*, int32_t*);
+                                          cudaStream_t, int*, int32_t*, const unsigned char*);
 
 template <typename T>
 cudaError_t launch_aba(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,

@@ -517,9 +517,10 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   st = ensure_ws(m, (size_t)slots * m->n * rd::aba_ws_per_link() * sizeof(T));
   if (st != RD_OK) return st;
   static const bool no_dh = getenv("RD_ABA_NODH") && getenv("RD_ABA_NODH")[0] == '1';   // A/B knob
-  cudaError_t e = (m->dh_ok && !m->has_prism && !no_dh)      // the DH ABA kernel is revolute-only
+  cudaError_t e = (m->dh_ok && !no_dh)
       ? rd::launch_aba_dh<T>(m->n, dh_dev<T>(m), dh_bnd<T>(m), batch, q, qd, tau, qdd,
-                             reinterpret_cast<T*>(m->ws), slots, s, &g_launches, status)
+                             reinterpret_cast<T*>(m->ws), slots, s, &g_launches, status,
+                             m->has_prism ? m->dPrism : nullptr)
       : rd::launch_aba<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
                           reinterpret_cast<T*>(m->ws), slots, s, &g_launches, status);
   if (e != cudaSuccess) return cuda_fail(e, "forward dynamics launch");

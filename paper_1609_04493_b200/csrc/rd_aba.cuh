@@ -172,17 +172,16 @@ __device__ __forceinline__ void gen_rot_plane(T* b, int i, int j, T c, T s) {
   }
 }
 template <typename T>
-__device__ __forceinline__ void dh_congruence(const LinkDH<T>& C, T s, T c, Sym6<T>& K) {
+__device__ __forceinline__ void dh_congruence(T ca, T sa, T p0, T p1, T p2, T s, T c, Sym6<T>& K) {
   // Rz(theta): plane (0, 1), fixed axis 2
   sym_rot_plane(K.a, 0, 1, 2, c, s);
   gen_rot_plane(K.b, 0, 1, c, s);
   sym_rot_plane(K.c, 0, 1, 2, c, s);
   // Rx(alpha): plane (1, 2), fixed axis 0
-  sym_rot_plane(K.a, 1, 2, 0, C.ca, C.sa);
-  gen_rot_plane(K.b, 1, 2, C.ca, C.sa);
-  sym_rot_plane(K.c, 1, 2, 0, C.ca, C.sa);
+  sym_rot_plane(K.a, 1, 2, 0, ca, sa);
+  gen_rot_plane(K.b, 1, 2, ca, sa);
+  sym_rot_plane(K.c, 1, 2, 0, ca, sa);
   // p-shift: B_new = B' - A'[p], C_new = C' + [p]B' + ([p]B')^T - [p]A'[p]
-  const T p0 = C.p0, p1 = C.p1, p2 = C.p2;
   T Ap[9];
   sym_full(K.a, Ap);
   T AP[9];
@@ -212,6 +211,10 @@ __device__ __forceinline__ void dh_congruence(const LinkDH<T>& C, T s, T c, Sym6
   K.c[3] += PB[1] + PB[3] - PAP[1];
   K.c[4] += PB[2] + PB[6] - PAP[2];
   K.c[5] += PB[5] + PB[7] - PAP[5];
+}
+template <typename T>
+__device__ __forceinline__ void dh_congruence(const LinkDH<T>& C, T s, T c, Sym6<T>& K) {
+  dh_congruence(C.ca, C.sa, C.p0, C.p1, C.p2, s, c, K);
 }
 
 template <typename T>

@@ -107,7 +107,8 @@ cudaError_t launch_rnea_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bn
 template <typename T>
 cudaError_t launch_aba_dh(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd,
                           int64_t B, const T* q, const T* qd, const T* tau, T* qdd,
-                          T* ws, int64_t ws_slots, cudaStream_t st, int* launches, int32_t* status);
+                          T* ws, int64_t ws_slots, cudaStream_t st, int* launches, int32_t* status,
+                          const unsigned char* prism = nullptr);
 template <typename T>
 cudaError_t launch_fd_scan(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                            int64_t B, const T* q, const T* qd, const T* tau, T* qdd, T* ws,

@@ -31,24 +31,6 @@ constexpr int kRevThreads = 128;
 #endif
 constexpr int kRevPD = RD_REV_PD, kRevU = RD_REV_U;
 
-// (sin, cos) of theta and the variable translation of link C: revolute theta =
-// th0 + q; prismatic (PR && prism) theta = th0, p = (p0, p1 - sa q, p2 + ca q).
-template <bool PR, typename T>
-__device__ __forceinline__ void dh_link(const LinkDH<T>& C, bool prism, T qi, T* s, T* c, T* p1, T* p2) {
-  const T qa = (PR && prism) ? T(0) : qi;
-  if (sizeof(T) == 8) {
-    rd_sincos(qa + C.th0, s, c);
-  } else {
-    T s0, c0;
-    rd_sincos(qa, &s0, &c0);
-    *s = fma(s0, C.cth0, c0 * C.sth0);
-    *c = fma(c0, C.cth0, -(s0 * C.sth0));
-  }
-  const T dq = (PR && prism) ? qi : T(0);
-  *p1 = PR ? fma(-C.sa, dq, C.p1) : C.p1;
-  *p2 = PR ? fma(C.ca, dq, C.p2) : C.p2;
-}
-
 template <typename T, bool PR>
 __global__ void __launch_bounds__(kRevThreads, 4)
 rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,

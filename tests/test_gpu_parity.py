@@ -264,6 +264,26 @@ def test_fd_aba_parity(rd, n):
     assert f < 1e-8
 
 
+@pytest.mark.parametrize("n,pf", [(12, 0.5), (60, 0.3)])
+def test_fd_aba_prismatic_dh(rd, n, pf):
+    # revolute + prismatic chains take the DH-frame ABA (prismatic instantiation)
+    r = synth.random_chain(n, 930 + n, prismatic_fraction=pf)
+    b, f = check_fd(rd, r, synth.GRAVITY_Z, 1500, 6)       # backward error <= 1e-10 inside (A14)
+    assert f < 1e-5                                        # forward error: cond(M)-limited (A14)
+
+
+def test_fd_aba_screw_joints_joint_frames(rd):
+    # a screw joint has no one-variable DH form: the joint-frame ABA kernel runs
+    r = synth.random_chain(9, 941, prismatic_fraction=0.3)
+    for i in range(9):
+        if np.linalg.norm(r["S"][i, 3:]) > 0.5:
+            r["S"][i, :3] += 0.15 * r["S"][i, 3:]
+            break
+    b, f = check_fd(rd, r, synth.GRAVITY_Z, 1500, 7)
+    assert f < 1e-7
+    b32, _ = check_fd(rd, r, synth.GRAVITY_Z, 500, 8, torch.float32, bwd_tol=1e-3)
+
+
 def test_fd_C4_sampled(rd):
     # Config C4: n = 100, 100k states (the bench launch); sampled backward-error check.
     cfg = synth.CONFIGS["C4"]
