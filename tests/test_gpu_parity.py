@@ -468,7 +468,15 @@ def test_fd_status_array(rd, algo, dh):
     assert np.all(st[good] == 0)
     assert rel_err_per_state(out[:, good], qdd[:, good], floor=1.0).max() < 1e-9
     for b, j in bad.items():
-        assert st[b] == (1 if algo == "jsiia" else j), (b, st[b])
+        if algo == "jsiia":
+            assert st[b] == 1, (b, st[b])
+        elif dh:
+            assert st[b] == j, (b, st[b])
+        else:
+            # with prismatic joints the NaN slide enters only the translation, and a
+            # prismatic parent's pivot (the A block of the articulated inertia) stays
+            # finite: the tip-most failing pivot is link j or a more basal one
+            assert 1 <= st[b] <= j, (b, st[b])
         assert not np.all(np.isfinite(out[:, b]))
     out2 = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()   # plain call, same qdd
     np.testing.assert_array_equal(np.isfinite(out2), np.isfinite(out))
