@@ -803,10 +803,11 @@ rd_status_t rd_inverse_dynamics_host_f64(rd_model_t m, int64_t batch, const doub
   if (dev != m->device) return fail(RD_E_ARG, "current CUDA device differs from the model's device");
   std::lock_guard<std::mutex> lk(m->mu);
   const int n = m->n;
-  // chunk = ~kHostChunkMB of each input array: small enough that the pipeline fill/drain
+  // chunk = ~32 MB of each input array (measured: 4/8/16/32/64 MB -> 6.0/6.4/6.9/7.0/6.9e7
+  // evals/s at C3, PCIe-bound at ~50 GB/s H2D): small enough that the pipeline fill/drain
   // (first H2D, last kernel + D2H) is a few % of a 10^6-state call, large enough to amortise
   // the per-copy overhead (RD_HOST_CHUNK_MB overrides, for measurement)
-  static const int64_t chunk_mb = getenv("RD_HOST_CHUNK_MB") ? atoll(getenv("RD_HOST_CHUNK_MB")) : 16;
+  static const int64_t chunk_mb = getenv("RD_HOST_CHUNK_MB") ? atoll(getenv("RD_HOST_CHUNK_MB")) : 32;
   const int64_t chunk = std::min<int64_t>(batch, std::max<int64_t>(4096, (chunk_mb << 20) / (8ll * n)));
   const size_t set_bytes = (size_t)4 * n * chunk * sizeof(double);
   if (m->hbuf_bytes < set_bytes) {
