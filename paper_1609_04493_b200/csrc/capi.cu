@@ -391,19 +391,25 @@ template <typename T> const rd::Boundary<T>& bnd(rd_model_t m);
 template <> const rd::Boundary<double>& bnd<double>(rd_model_t m) { return m->b64; }
 template <> const rd::Boundary<float>& bnd<float>(rd_model_t m) { return m->b32; }
 
-// Strategy table (measured on B200, profiles/r01):
-//  * batch <= kWarpScanMaxBatch and n <= 32 -> WARP_SCAN: one warp per state,
-//    lane = link, log-depth shuffle scans; the latency regime (paper P:505/P:524),
-//    e.g. n = 30, B = 1..1000: 21-24 us vs 43-49 us for THREAD;
-//  * otherwise THREAD when the on-chip stash fits (n <= 30 fp64 / 32 fp32, every
-//    joint revolute with zero pitch or prismatic): 3.9x faster than WARP_SCAN at B = 1M;
-//  * otherwise GENERIC (any n, any joint type).
-//  * 32 < n <= 512 and batch <= kBlockScanMaxBatch -> BLOCK_SCAN: one CTA per
-//    state (NEXT-3), e.g. n = 512, B = 1: 29 us vs 262 us (REVERSE), 687 us (GENERIC);
-//  * longer revolute/prismatic chains at larger batch -> REVERSE (stash-free), else
-//    (screw joints) GENERIC.
-constexpr int64_t kWarpScanMaxBatch = 4096;
+// Strategy table (measured on B200: profiles/r01/
+// crossover.csv, latency.csv, sweep_*.csv).  DH chains (revolute / prismatic):
+//  * n >= 20 (n <= 32) and batch <= 2048 -> WARP_SCAN: one warp per state, lane =
+//    link, log-depth shuffle scans; the latency regime (paper P:505/P:524), e.g.
+//    n = 30, B = 2048: 26 us vs 29 us (REVERSE) and 39 us (THREAD);
+//  * batch above the thread crossover (fp64 32768, fp32 49152) and the on-chip
+//    stash fits (n <= 30 fp64 / 32 fp32) -> THREAD: e.g. n = 30, B = 1M: 3.9x
+//    WARP_SCAN; below it one tile per SM is latency-bound (2n serial link steps),
+//    and the 16-warp stash-free REVERSE wins (n = 30, B = 16384: 30 vs 39 us);
+//  * n > 32 and batch <= 1024 -> BLOCK_SCAN: one CTA per state (NEXT-3), e.g.
+//    n = 512, B = 1: 29 us vs 213 us (REVERSE), 650 us (GENERIC);
+//  * otherwise REVERSE.
+// Screw joints (no DH form): WARP_SCAN for n <= 32 and batch <= 4096, BLOCK_SCAN
+// for longer chains and batch <= 1024, else GENERIC.
+constexpr int64_t kWarpScanMaxBatch = 4096;     // joint-frame chains
+constexpr int64_t kWarpScanMaxBatchDH = 2048;   // DH chains, n >= kWarpScanMinN
+constexpr int kWarpScanMinN = 20;
 constexpr int64_t kBlockScanMaxBatch = 1024;
+constexpr int64_t kThreadMinBatch64 = 32768, kThreadMinBatch32 = 49152;
 
 rd_strategy_t resolve(rd_model_t m, int64_t batch, bool fp64) {
   const bool thread_ok = m->dh_ok && rd::thread_kernel_has_n(m->n, fp64);
@@ -418,10 +424,16 @@ rd_strategy_t resolve(rd_model_t m, int64_t batch, bool fp64) {
     case RD_STRAT_WARP_SCAN_EQ15: return warp_ok ? RD_STRAT_WARP_SCAN_EQ15 : RD_STRAT_GENERIC;
     default: break;
   }
+  const bool block_ok = !warp_ok && m->n <= 512 && batch <= kBlockScanMaxBatch;
+  if (m->dh_ok) {
+    if (warp_ok && m->n >= kWarpScanMinN && batch <= kWarpScanMaxBatchDH) return RD_STRAT_WARP_SCAN;
+    if (thread_ok && batch > (fp64 ? kThreadMinBatch64 : kThreadMinBatch32)) return RD_STRAT_THREAD;
+    if (block_ok) return RD_STRAT_BLOCK_SCAN;
+    return RD_STRAT_REVERSE;
+  }
   if (warp_ok && batch <= kWarpScanMaxBatch) return RD_STRAT_WARP_SCAN;
-  if (!warp_ok && m->n <= 512 && batch <= kBlockScanMaxBatch) return RD_STRAT_BLOCK_SCAN;
-  if (thread_ok) return RD_STRAT_THREAD;
-  return m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
+  if (block_ok) return RD_STRAT_BLOCK_SCAN;
+  return RD_STRAT_GENERIC;
 }
 
 template <typename T>

@@ -125,6 +125,23 @@ def test_ragged_batches(rd, B):
         check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strat)
 
 
+def test_auto_strategy_table(rd):
+    # the measured AUTO table (csrc/capi.cu resolve())
+    dh30 = rd.Model.from_robot(synth.random_chain(30, 1030), synth.GRAVITY_Z)
+    dh10 = rd.Model.from_robot(synth.random_chain(10, 1010), synth.GRAVITY_Z)
+    dh100 = rd.Model.from_robot(synth.random_chain(100, 1100), synth.GRAVITY_Z)
+    screw = synth.random_chain(12, 77)
+    screw["S"][0, :3] += 0.2 * screw["S"][0, 3:]
+    sc = rd.Model.from_robot(screw, synth.GRAVITY_Z)
+    for model, B, fp64, want in [(dh30, 1000, True, "warp_scan"), (dh30, 16384, True, "reverse"),
+                                 (dh30, 1_000_000, True, "thread"), (dh30, 40000, False, "reverse"),
+                                 (dh30, 60000, False, "thread"), (dh10, 1000, True, "reverse"),
+                                 (dh10, 100_000, True, "thread"), (dh100, 64, True, "block_scan"),
+                                 (dh100, 100_000, True, "reverse"), (sc, 1000, True, "warp_scan"),
+                                 (sc, 100_000, True, "generic")]:
+        assert model.resolve_strategy(B, fp64) == want, (model.n, B, fp64, want)
+
+
 def test_empty_batch_is_noop(rd):
     model = rd.Model.from_robot(synth.random_chain(6, 1), synth.GRAVITY_Z)
     z = torch.empty((6, 0), dtype=torch.float64, device="cuda")
