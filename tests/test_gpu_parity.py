@@ -142,6 +142,29 @@ def test_auto_strategy_table(rd):
         assert model.resolve_strategy(B, fp64) == want, (model.n, B, fp64, want)
 
 
+@pytest.mark.parametrize("strategy", ["thread", "warp_scan", "reverse", "generic"])
+def test_parity_check_fails_on_corrupted_operand(rd, strategy):
+    # fault injection: one model operand off by 1e-7 relative (a link mass,
+    # a home translation) must be caught by the parity metric at the 1e-10 bar
+    r = synth.random_chain(12, 1212)
+    q, qd, qdd = synth.states(15, 12, 0, 700)
+    ref = oracle.rnea_batch(r, synth.GRAVITY_Z, q, qd, qdd)
+    for corrupt in ("mass", "translation"):
+        bad = {k: v.copy() for k, v in r.items()}
+        if corrupt == "mass":
+            bad["J"][5] *= 1 + 1e-7
+        else:
+            bad["M"][7, 0, 3] *= 1 + 1e-7
+        model = rd.Model.from_robot(bad, synth.GRAVITY_Z)
+        model.set_strategy(strategy)
+        tau, _ = run_id(rd, model, q, qd, qdd)
+        assert rel_err_per_state(tau, ref).max() > 1e-9, corrupt
+    model = rd.Model.from_robot(r, synth.GRAVITY_Z)          # and the clean model passes
+    model.set_strategy(strategy)
+    tau, _ = run_id(rd, model, q, qd, qdd)
+    assert rel_err_per_state(tau, ref).max() <= 1e-10
+
+
 def test_empty_batch_is_noop(rd):
     model = rd.Model.from_robot(synth.random_chain(6, 1), synth.GRAVITY_Z)
     z = torch.empty((6, 0), dtype=torch.float64, device="cuda")
