@@ -17,6 +17,7 @@
 //  * the loops are rolled (unroll 2): the whole kernel stays in the instruction
 //    cache (a fully unrolled n = 30 body thrashed it, profiles/r01).
 #include <cuda_runtime.h>
+#include <type_traits>
 #include <cstdint>
 #include <cstdlib>
 #include "rd_internal.h"
@@ -141,6 +142,9 @@ template <> struct TmemIO<float> {
 #endif
 #ifndef RD_TAU_DEFER
 #define RD_TAU_DEFER 1
+#endif
+#ifndef RD_STASH_VEC
+#define RD_STASH_VEC 1
 #endif
 template <typename T, int W> struct StepCfg { static constexpr int kPD = 2, kUnroll = 1; };
 template <> struct StepCfg<double, 8> { static constexpr int kPD = RD_PD64, kUnroll = RD_U64; };
@@ -315,7 +319,6 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
   constexpr int kColsPerWarp = 2048 / W;
   constexpr int KC = TmemIO<T>::kCols;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sstash = reinterpret_cast<T*>(smem_raw);     // slots lt..n-1: [slot - lt][8][NT]
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5;
   const int tid = threadIdx.x;
@@ -327,6 +330,37 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
   const int n = P.n, lt = P.lt;
   const int64_t ntiles = (B + NT - 1) / NT;
   const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+#if RD_STASH_VEC
+  // 16-byte vectors: [slot - lt][8 / VW][NT] of (double2 | float4) -- conflict-free
+  // (consecutive threads 16 B apart), 2 (fp32) / 4 (fp64) shared-memory
+  // instructions per slot instead of 8 (the fp32 kernel is issue-bound)
+  using V16 = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+  constexpr int VW = 16 / sizeof(T), NV = 8 / VW;
+  V16* vstash = reinterpret_cast<V16*>(smem_raw);
+  auto vptr = [&](int slot) { return vstash + (size_t)(slot - lt) * NV * NT + tid; };
+  auto put_smem = [&](int slot, const T* st) {
+    V16* d = vptr(slot);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      V16 v;
+      T* e = reinterpret_cast<T*>(&v);
+#pragma unroll
+      for (int j = 0; j < VW; ++j) e[j] = st[k * VW + j];
+      d[k * NT] = v;
+    }
+  };
+  auto get_smem = [&](int slot, T* cur) {
+    const V16* d = vptr(slot);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const V16 v = d[k * NT];
+      const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+      for (int j = 0; j < VW; ++j) cur[k * VW + j] = e[j];
+    }
+  };
+#else
+  T* sstash = reinterpret_cast<T*>(smem_raw);     // slots lt..n-1: [slot - lt][8][NT]
   auto sptr = [&](int slot) { return sstash + (size_t)(slot - lt) * 8 * NT + tid; };
   auto put_smem = [&](int slot, const T* st) {
     T* d = sptr(slot);
@@ -338,6 +372,7 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
 #pragma unroll
     for (int k = 0; k < 8; ++k) cur[k] = d[k * NT];
   };
+#endif
   auto put_any = [&](int slot, const T* st) {
     if (slot < lt) TmemIO<T>::st(tbase + (uint32_t)(slot * KC), st);
     else put_smem(slot, st);
