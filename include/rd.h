@@ -147,6 +147,28 @@ rd_status_t rd_model_set_fd_algo(rd_model_t m, rd_fd_algo_t algo);
  * <= 0 in the ABI sweep, Eq. 7; JSIIA: the first non-positive Cholesky pivot of
  * M(q)).  A failing state's qdd is NaN and other states are unaffected.
  * status must be 4-byte aligned device memory not overlapping qdd (RD_E_ARG). */
+/* Per-state boundary data (NEXT-4; the full signature of Eq. (3)/(4), P:79-92,
+ * with V_0, Vdot_0, F_{n+1} varying per state): V0, Vdot0 (base frame) and Ftip
+ * (acting on link n, in the user's link-n frame; f_{n,n+1} = I, A5) are DEVICE
+ * arrays of layout [6][batch], component-major (x[k*batch + b]); any of them
+ * NULL = the model's value (gravity / rd_model_set_boundary).  Same alignment /
+ * device / aliasing rules as the state arrays (RD_E_ARG).  ID runs on THREAD,
+ * WARP_SCAN, GENERIC or REVERSE (AUTO picks among them; an explicit
+ * WARP_SCAN_EQ13/EQ15 strategy -> RD_E_UNSUPPORTED); FD on ABA only (other FD
+ * algorithms -> RD_E_UNSUPPORTED).  status as in rd_forward_dynamics_ex_*. */
+rd_status_t rd_inverse_dynamics_bnd_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                        const double* qdd, const double* V0, const double* Vdot0,
+                                        const double* Ftip, double* tau, void* stream);
+rd_status_t rd_inverse_dynamics_bnd_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,
+                                        const float* qdd, const float* V0, const float* Vdot0,
+                                        const float* Ftip, float* tau, void* stream);
+rd_status_t rd_forward_dynamics_bnd_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                        const double* tau, const double* V0, const double* Vdot0,
+                                        const double* Ftip, double* qdd, int32_t* status, void* stream);
+rd_status_t rd_forward_dynamics_bnd_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,
+                                        const float* tau, const float* V0, const float* Vdot0,
+                                        const float* Ftip, float* qdd, int32_t* status, void* stream);
+
 rd_status_t rd_forward_dynamics_ex_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
                                        const double* tau, double* qdd, int32_t* status, void* stream);
 rd_status_t rd_forward_dynamics_ex_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,

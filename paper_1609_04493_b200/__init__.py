@@ -36,6 +36,8 @@ EXPORTS = [
     "rd_inverse_dynamics_f64", "rd_inverse_dynamics_f32", "rd_forward_dynamics_f64",
     "rd_forward_dynamics_f32", "rd_model_set_fd_algo", "rd_inverse_dynamics_host_f64",
     "rd_last_launch_count", "rd_forward_dynamics_ex_f64", "rd_forward_dynamics_ex_f32",
+    "rd_inverse_dynamics_bnd_f64", "rd_inverse_dynamics_bnd_f32", "rd_forward_dynamics_bnd_f64",
+    "rd_forward_dynamics_bnd_f32",
 ]
 
 
@@ -71,6 +73,10 @@ def lib():
             getattr(L, name).argtypes = [vp, i64, vp, vp, vp, vp, vp]
         for name in ("rd_forward_dynamics_ex_f64", "rd_forward_dynamics_ex_f32"):
             getattr(L, name).argtypes = [vp, i64, vp, vp, vp, vp, vp, vp]
+        for name in ("rd_inverse_dynamics_bnd_f64", "rd_inverse_dynamics_bnd_f32"):
+            getattr(L, name).argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]
+        for name in ("rd_forward_dynamics_bnd_f64", "rd_forward_dynamics_bnd_f32"):
+            getattr(L, name).argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.rd_inverse_dynamics_host_f64.argtypes = [vp, i64, vp, vp, vp, vp]
         L.rd_last_launch_count.restype = i32
         for name in EXPORTS:
@@ -169,29 +175,65 @@ def _check_tensors(model: Model, *ts):
     return t0.dtype
 
 
-def inverse_dynamics(model: Model, q, qd, qdd, out=None, stream=None):
-    """tau = ID(q, qd, qdd) (Eq. 1-3) for B states; torch CUDA tensors [n, B]."""
+def _boundary_ptrs(boundary, ref):
+    """(V0, Vdot0, Ftip) per-state arrays [6, B] (None entries allowed) -> pointers."""
+    ptrs = []
+    for t in boundary:
+        if t is None:
+            ptrs.append(None)
+            continue
+        if t.dtype != ref.dtype or t.device != ref.device or tuple(t.shape) != (6, ref.shape[1]) \
+                or not t.is_contiguous():
+            raise RdError("boundary arrays must be contiguous [6, B] tensors with the inputs' dtype/device")
+        ptrs.append(t.data_ptr())
+    if len(ptrs) != 3:
+        raise RdError("boundary = (V0, Vdot0, Ftip)")
+    return ptrs
+
+
+def inverse_dynamics(model: Model, q, qd, qdd, out=None, stream=None, boundary=None):
+    """tau = ID(q, qd, qdd) (Eq. 1-3) for B states; torch CUDA tensors [n, B].
+
+    boundary: optional per-state (V0, Vdot0, Ftip), each a [6, B] tensor or None
+    (rd_inverse_dynamics_bnd_*); None = the model's boundary."""
     import torch
     dt = _check_tensors(model, q, qd, qdd)
     if out is None:
         out = torch.empty_like(q)
     _check_tensors(model, q, out)
+    if boundary is not None:
+        v0, vd0, ft = _boundary_ptrs(boundary, q)
+        f = lib().rd_inverse_dynamics_bnd_f64 if dt == torch.float64 else lib().rd_inverse_dynamics_bnd_f32
+        _check(f(model.handle, q.shape[1], q.data_ptr(), qd.data_ptr(), qdd.data_ptr(), v0, vd0, ft,
+                 out.data_ptr(), _stream_ptr(stream)), "rd_inverse_dynamics_bnd")
+        return out
     f = lib().rd_inverse_dynamics_f64 if dt == torch.float64 else lib().rd_inverse_dynamics_f32
     _check(f(model.handle, q.shape[1], q.data_ptr(), qd.data_ptr(), qdd.data_ptr(), out.data_ptr(),
              _stream_ptr(stream)), "rd_inverse_dynamics")
     return out
 
 
-def forward_dynamics(model: Model, q, qd, tau, out=None, stream=None, status=None):
+def forward_dynamics(model: Model, q, qd, tau, out=None, stream=None, status=None, boundary=None):
     """qdd = FD(q, qd, tau) (Eq. 4, ABA Eq. 7-8) for B states; torch CUDA tensors [n, B].
 
     status: optional int32 CUDA tensor [B] (rd_forward_dynamics_ex_*): 0, or the
-    1-based link of the failing pivot of that state (its qdd is NaN)."""
+    1-based link of the failing pivot of that state (its qdd is NaN).
+    boundary: optional per-state (V0, Vdot0, Ftip) as in inverse_dynamics (ABA only)."""
     import torch
     dt = _check_tensors(model, q, qd, tau)
     if out is None:
         out = torch.empty_like(q)
     _check_tensors(model, q, out)
+    if status is not None and (status.dtype != torch.int32 or status.device != q.device
+                               or status.shape != (q.shape[1],) or not status.is_contiguous()):
+        raise RdError("status must be a contiguous int32 [B] tensor on the inputs' device")
+    if boundary is not None:
+        v0, vd0, ft = _boundary_ptrs(boundary, q)
+        f = lib().rd_forward_dynamics_bnd_f64 if dt == torch.float64 else lib().rd_forward_dynamics_bnd_f32
+        _check(f(model.handle, q.shape[1], q.data_ptr(), qd.data_ptr(), tau.data_ptr(), v0, vd0, ft,
+                 out.data_ptr(), status.data_ptr() if status is not None else None, _stream_ptr(stream)),
+               "rd_forward_dynamics_bnd")
+        return out
     if status is None:
         f = lib().rd_forward_dynamics_f64 if dt == torch.float64 else lib().rd_forward_dynamics_f32
         _check(f(model.handle, q.shape[1], q.data_ptr(), qd.data_ptr(), tau.data_ptr(), out.data_ptr(),

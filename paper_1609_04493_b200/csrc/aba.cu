@@ -50,11 +50,12 @@ constexpr int kAbaPerLink = 7;   // Ubar = U/D (6), ubar = u/D
 constexpr int kAbaThreads = 128;
 int aba_ws_per_link() { return kAbaPerLink; }
 
-template <typename T>
+template <typename T, bool SB>
 __global__ void __launch_bounds__(kAbaThreads)
 aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int64_t B,
            const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ tau_in,
-           T* __restrict__ qdd_out, T* __restrict__ ws, int64_t slots, int32_t* __restrict__ status) {
+           T* __restrict__ qdd_out, T* __restrict__ ws, int64_t slots, int32_t* __restrict__ status,
+           const typename SBArg<T, SB>::type sb) {
   const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= slots) return;
   const T zero6[6] = {0, 0, 0, 0, 0, 0};
@@ -63,6 +64,9 @@ aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int
     T V[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) V[k] = bnd.V0[k];
+    if constexpr (SB) {                              // per-state V_0 (NEXT-4)
+      if (sb.V0) sb_vec(sb.V0, sb.A0, B, b, V);
+    }
     for (int i = 0; i < n; ++i) {
       const LinkConst<T> C = L[i];
       Rot<T> R;
@@ -83,6 +87,9 @@ aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int
     int fail = 0;                                         // tip-most link with Omega <= 0 (1-based)
 #pragma unroll
     for (int k = 0; k < 6; ++k) pc[k] = bnd.Ftip[k];   // F_{n+1} enters link n like a bias wrench
+    if constexpr (SB) {
+      if (sb.Ft) sb_vec(sb.Ft, sb.At, B, b, pc);
+    }
 #pragma unroll
     for (int k = 0; k < 6; ++k) { Kc.a[k] = 0; Kc.c[k] = 0; }
 #pragma unroll
@@ -154,6 +161,10 @@ aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int
     T a[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) { a[k] = bnd.Vd0[k]; V[k] = bnd.V0[k]; }
+    if constexpr (SB) {
+      if (sb.V0) sb_vec(sb.V0, sb.A0, B, b, V);
+      if (sb.Vd0) sb_vec(sb.Vd0, sb.A0, B, b, a);
+    }
     for (int i = 0; i < n; ++i) {
       const LinkConst<T> C = L[i];
       const T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
@@ -194,12 +205,12 @@ aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int
 // 22-flop Ad maps.  Revolute S = (0, e_z): U = Jhat[:, 5], D = U[5],
 // u = tau - phat[5]; prismatic (PR instantiation, per-link flag) S = (e_z, 0):
 // U = Jhat[:, 2], D = U[2], u = tau - phat[2], d = d0 + q.
-template <typename T, int MB, bool PR>
+template <typename T, int MB, bool PR, bool SB>
 __global__ void __launch_bounds__(kAbaThreads, MB)
 aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
               const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ tau_in,
               T* __restrict__ qdd_out, T* __restrict__ ws, int64_t slots, int32_t* __restrict__ status,
-              const unsigned char* __restrict__ prism_g) {
+              const unsigned char* __restrict__ prism_g, const typename SBArg<T, SB>::type sb) {
   // model constants staged in shared memory (broadcast reads, no long-scoreboard waits)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LinkDH<T>* L = reinterpret_cast<LinkDH<T>*>(smem_raw);
@@ -219,6 +230,9 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
     T V[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) V[k] = bnd.V0[k];
+    if constexpr (SB) {                              // per-state V_0 (NEXT-4)
+      if (sb.V0) sb_vec(sb.V0, sb.A0, B, b, V);
+    }
     // sweep 1: V_n only; inputs kS1PD links ahead
     {
       T aq[kS1PD], aqd[kS1PD];
@@ -260,6 +274,9 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
     int fail = 0;                                         // tip-most link with Omega <= 0 (1-based)
 #pragma unroll
     for (int k = 0; k < 6; ++k) { pc[k] = bnd.Ftip[k]; Kc.a[k] = 0; Kc.c[k] = 0; }
+    if constexpr (SB) {
+      if (sb.Ft) sb_vec(sb.Ft, sb.At, B, b, pc);
+    }
 #pragma unroll
     for (int k = 0; k < 9; ++k) Kc.b[k] = 0;
     // sweep 2 (backward); inputs one link ahead (each iteration is long)
@@ -338,6 +355,10 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
     T a[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) { a[k] = bnd.Vd0[k]; V[k] = bnd.V0[k]; }
+    if constexpr (SB) {
+      if (sb.V0) sb_vec(sb.V0, sb.A0, B, b, V);
+      if (sb.Vd0) sb_vec(sb.Vd0, sb.A0, B, b, a);
+    }
     {
       T bq[kS3PD], bqd[kS3PD];
 #pragma unroll
@@ -426,52 +447,69 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
   }
 }
 
-template <typename T, bool PR>
+template <typename T, bool PR, bool SB>
 static cudaError_t launch_aba_dh_pr(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B,
                                     const T* q, const T* qd, const T* tau, T* qdd, T* ws, int64_t ws_slots,
-                                    cudaStream_t st, int32_t* status, const unsigned char* prism) {
+                                    cudaStream_t st, int32_t* status, const unsigned char* prism,
+                                    const typename SBArg<T, SB>::type& sb) {
   const int64_t grid = (ws_slots + kAbaThreads - 1) / kAbaThreads;
   const size_t smem = (size_t)n * sizeof(LinkDH<T>) + (PR ? (size_t)n : 0);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(aba_dh_kernel<T, 3, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(aba_dh_kernel<T, 3, PR, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  aba_dh_kernel<T, 3, PR><<<(unsigned)grid, kAbaThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws,
-                                                                      ws_slots, status, prism);
+  aba_dh_kernel<T, 3, PR, SB><<<(unsigned)grid, kAbaThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws,
+                                                                          ws_slots, status, prism, sb);
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_aba_dh(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                           const T* qd, const T* tau, T* qdd, T* ws, int64_t ws_slots, cudaStream_t st,
-                          int* launches, int32_t* status, const unsigned char* prism) {
+                          int* launches, int32_t* status, const unsigned char* prism,
+                          const StateBoundary<T>* sb) {
   ++*launches;
-  return prism ? launch_aba_dh_pr<T, true>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots, st, status, prism)
-               : launch_aba_dh_pr<T, false>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots, st, status, nullptr);
+  const NoStateBoundary nsb{};
+  if (sb)
+    return prism ? launch_aba_dh_pr<T, true, true>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots, st, status,
+                                                   prism, *sb)
+                 : launch_aba_dh_pr<T, false, true>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots, st, status,
+                                                    nullptr, *sb);
+  return prism ? launch_aba_dh_pr<T, true, false>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots, st, status,
+                                                  prism, nsb)
+               : launch_aba_dh_pr<T, false, false>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots, st, status,
+                                                   nullptr, nsb);
 }
 template cudaError_t launch_aba_dh<double>(int, const LinkDH<double>*, const Boundary<double>&, int64_t,
                                            const double*, const double*, const double*, double*, double*, int64_t,
-                                           cudaStream_t, int*, int32_t*, const unsigned char*);
+                                           cudaStream_t, int*, int32_t*, const unsigned char*,
+                                           const StateBoundary<double>*);
 template cudaError_t launch_aba_dh<float>(int, const LinkDH<float>*, const Boundary<float>&, int64_t,
                                           const float*, const float*, const float*, float*, float*, int64_t,
-                                          cudaStream_t, int*, int32_t*, const unsigned char*);
+                                          cudaStream_t, int*, int32_t*, const unsigned char*,
+                                          const StateBoundary<float>*);
 
 template <typename T>
 cudaError_t launch_aba(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                        const T* qd, const T* tau, T* qdd, T* ws, int64_t ws_slots, cudaStream_t st,
-                       int* launches, int32_t* status) {
+                       int* launches, int32_t* status, const StateBoundary<T>* sb) {
   const int64_t grid = (ws_slots + kAbaThreads - 1) / kAbaThreads;
-  aba_kernel<T><<<(unsigned)grid, kAbaThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots, status);
+  if (sb)
+    aba_kernel<T, true><<<(unsigned)grid, kAbaThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots,
+                                                                 status, *sb);
+  else
+    aba_kernel<T, false><<<(unsigned)grid, kAbaThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws, ws_slots,
+                                                                  status, NoStateBoundary{});
   ++*launches;
   return cudaGetLastError();
 }
 
 template cudaError_t launch_aba<double>(int, const LinkConst<double>*, const Boundary<double>&, int64_t,
                                         const double*, const double*, const double*, double*, double*, int64_t,
-                                        cudaStream_t, int*, int32_t*);
+                                        cudaStream_t, int*, int32_t*, const StateBoundary<double>*);
 template cudaError_t launch_aba<float>(int, const LinkConst<float>*, const Boundary<float>&, int64_t,
                                        const float*, const float*, const float*, float*, float*, int64_t,
-                                       cudaStream_t, int*, int32_t*);
+                                       cudaStream_t, int*, int32_t*, const StateBoundary<float>*);
 
 }  // namespace rd

@@ -159,6 +159,8 @@ struct rd_model_s {
   double V0[6] = {0}, Vd0[6] = {0}, Ftip_user[6] = {0};
   rd::Boundary<double> b64;
   rd::Boundary<float> b32;
+  double sbA0dh[36] = {0};         // per-state boundary: user base twist -> DH base frame
+  double sbAt[36] = {0};           // per-state boundary: user frame-n wrench -> kernel frame n
   rd::LinkConst<double>* dL64 = nullptr;
   rd::LinkConst<float>* dL32 = nullptr;
   void* ws = nullptr;              // generic/FD workspace (device)
@@ -178,6 +180,8 @@ void rebuild_boundary(rd_model_t m) {
   // is expressed in link n's joint frame: F' = Ad_{T_n}^T F (power pairing).
   Mat6 A;
   adjoint(m->T[m->n - 1], A);
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 6; ++j) m->sbAt[6 * j + i] = A[i][j];    // F' = A^T F
   double Ft[6];
   for (int j = 0; j < 6; ++j) {
     double s = 0;
@@ -197,6 +201,8 @@ void rebuild_boundary(rd_model_t m) {
     // the last DH frame equals link n's joint frame, so F_{n+1} is unchanged.
     Mat6 Ai;
     adjoint(rigid_inv(m->D0), Ai);
+    for (int i = 0; i < 6; ++i)
+      for (int j = 0; j < 6; ++j) m->sbA0dh[6 * i + j] = Ai[i][j];
     for (int j = 0; j < 6; ++j) {
       double sv = 0, sa = 0;
       for (int k = 0; k < 6; ++k) { sv += Ai[j][k] * m->V0[k]; sa += Ai[j][k] * m->Vd0[k]; }
@@ -436,23 +442,71 @@ rd_strategy_t resolve(rd_model_t m, int64_t batch, bool fp64) {
   return RD_STRAT_GENERIC;
 }
 
+// Per-state boundary arrays (NEXT-4): validated device arrays [6][batch] -> the
+// kernel-side StateBoundary for joint-frame (jf) and DH kernels.
+struct UserStateBoundary {
+  const void* V0;
+  const void* Vd0;
+  const void* Ft;
+};
+template <typename T>
+rd_status_t check_state_boundary(rd_model_t m, int64_t batch, const UserStateBoundary& u, const T* out) {
+  const void* p[3] = {u.V0, u.Vd0, u.Ft};
+  const char* names[3] = {"V0", "Vdot0", "Ftip"};
+  const size_t bytes = (size_t)6 * batch * sizeof(T), ob = (size_t)m->n * batch * sizeof(T);
+  for (int k = 0; k < 3; ++k) {
+    if (!p[k]) continue;
+    if (reinterpret_cast<uintptr_t>(p[k]) % sizeof(T) != 0) return fail(RD_E_ARG, std::string("misaligned pointer: ") + names[k]);
+    if (!is_device_ptr(reinterpret_cast<const T*>(p[k]))) return fail(RD_E_ARG, std::string("not device memory: ") + names[k]);
+    const char* lo = reinterpret_cast<const char*>(p[k]);
+    const char* o = reinterpret_cast<const char*>(out);
+    if (lo < o + ob && o < lo + bytes) return fail(RD_E_ARG, std::string("output aliases ") + names[k]);
+  }
+  return RD_OK;
+}
+template <typename T>
+void make_state_boundary(rd_model_t m, const UserStateBoundary& u, bool dh, rd::StateBoundary<T>* sb) {
+  sb->V0 = reinterpret_cast<const T*>(u.V0);
+  sb->Vd0 = reinterpret_cast<const T*>(u.Vd0);
+  sb->Ft = reinterpret_cast<const T*>(u.Ft);
+  for (int i = 0; i < 36; ++i) {
+    sb->A0[i] = dh ? (T)m->sbA0dh[i] : (T)((i % 7) == 0 ? 1.0 : 0.0);   // joint frames: T_0 = I
+    sb->At[i] = (T)m->sbAt[i];                                        // last DH frame = joint frame n
+  }
+}
+
 template <typename T>
 rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* qd, const T* qdd, T* tau,
-                             void* stream) {
+                             void* stream, const UserStateBoundary* usb = nullptr) {
   g_launches = 0;
   rd_status_t st = check_io<T>(m, batch, q, qd, qdd, tau, true);
   if (st != RD_OK || batch == 0) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   rd_strategy_t strat = resolve(m, batch, sizeof(T) == 8);
+  rd::StateBoundary<T> sbj, sbd;                 // joint-frame / DH variants
+  const rd::StateBoundary<T>* pj = nullptr;
+  const rd::StateBoundary<T>* pd = nullptr;
+  if (usb) {
+    st = check_state_boundary<T>(m, batch, *usb, tau);
+    if (st != RD_OK) return st;
+    make_state_boundary<T>(m, *usb, false, &sbj);
+    make_state_boundary<T>(m, *usb, true, &sbd);
+    pj = &sbj;
+    pd = &sbd;
+    if (strat == RD_STRAT_BLOCK_SCAN) strat = m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
+    if (strat == RD_STRAT_WARP_SCAN_EQ13 || strat == RD_STRAT_WARP_SCAN_EQ15)
+      return fail(RD_E_UNSUPPORTED, "per-state boundary data: strategies THREAD, WARP_SCAN, GENERIC, REVERSE only");
+  }
   cudaError_t e = cudaSuccess;
   if (strat == RD_STRAT_THREAD) {
     bool ok = false;
     e = rd::launch_rnea_thread<T>(m->n, dh_consts<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok,
-                                  m->prism_mask);
-    if (!ok) strat = RD_STRAT_GENERIC;
+                                  m->prism_mask, pd);
+    if (!ok) strat = m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
   } else if (strat == RD_STRAT_WARP_SCAN) {
     bool ok = false;
-    e = rd::launch_rnea_warp<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok);
+    e = rd::launch_rnea_warp<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok,
+                                nullptr, pj);
     if (!ok) strat = RD_STRAT_GENERIC;
   }
   if (strat == RD_STRAT_WARP_SCAN_EQ13) {
@@ -472,7 +526,7 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   }
   if (strat == RD_STRAT_REVERSE) {
     e = rd::launch_rnea_rev<T>(m->n, dh_dev<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches,
-                               m->has_prism ? m->dPrism : nullptr);
+                               m->has_prism ? m->dPrism : nullptr, pd);
   }
   if (strat == RD_STRAT_GENERIC) {
     std::lock_guard<std::mutex> lk(m->mu);
@@ -480,7 +534,7 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     st = ensure_ws(m, (size_t)slots * m->n * rd::generic_ws_per_link() * sizeof(T));
     if (st != RD_OK) return st;
     e = rd::launch_rnea_generic<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau,
-                                   reinterpret_cast<T*>(m->ws), slots, s, &g_launches);
+                                   reinterpret_cast<T*>(m->ws), slots, s, &g_launches, pj);
   }
   if (e != cudaSuccess) return cuda_fail(e, "inverse dynamics launch");
   return RD_OK;
@@ -488,7 +542,7 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
 
 template <typename T>
 rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* qd, const T* tau, T* qdd,
-                             void* stream, int32_t* status = nullptr) {
+                             void* stream, int32_t* status = nullptr, const UserStateBoundary* usb = nullptr) {
   g_launches = 0;
   rd_status_t st = check_io<T>(m, batch, q, qd, tau, qdd, true);
   if (st != RD_OK || batch == 0) return st;
@@ -501,6 +555,14 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     if (so < qo + qb && qo < so + sb) return fail(RD_E_ARG, "status aliases qdd");
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  rd::StateBoundary<T> sbj, sbd;
+  if (usb) {
+    st = check_state_boundary<T>(m, batch, *usb, qdd);
+    if (st != RD_OK) return st;
+    if (m->fd_algo != RD_FD_ABA) return fail(RD_E_UNSUPPORTED, "per-state boundary data: FD algorithm ABA only");
+    make_state_boundary<T>(m, *usb, false, &sbj);
+    make_state_boundary<T>(m, *usb, true, &sbd);
+  }
   if (m->fd_algo == RD_FD_JSIIA) {
     bool ok = false;
     cudaError_t e = rd::launch_jsiia<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd, s,
@@ -532,9 +594,9 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   cudaError_t e = (m->dh_ok && !no_dh)
       ? rd::launch_aba_dh<T>(m->n, dh_dev<T>(m), dh_bnd<T>(m), batch, q, qd, tau, qdd,
                              reinterpret_cast<T*>(m->ws), slots, s, &g_launches, status,
-                             m->has_prism ? m->dPrism : nullptr)
+                             m->has_prism ? m->dPrism : nullptr, usb ? &sbd : nullptr)
       : rd::launch_aba<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
-                          reinterpret_cast<T*>(m->ws), slots, s, &g_launches, status);
+                          reinterpret_cast<T*>(m->ws), slots, s, &g_launches, status, usb ? &sbj : nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "forward dynamics launch");
   return RD_OK;
 }
@@ -792,6 +854,30 @@ rd_status_t rd_forward_dynamics_f64(rd_model_t m, int64_t batch, const double* q
 rd_status_t rd_forward_dynamics_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,
                                     const float* tau, float* qdd, void* stream) {
   return forward_dynamics<float>(m, batch, q, qd, tau, qdd, stream);
+}
+rd_status_t rd_inverse_dynamics_bnd_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                        const double* qdd, const double* V0, const double* Vdot0,
+                                        const double* Ftip, double* tau, void* stream) {
+  const UserStateBoundary u{V0, Vdot0, Ftip};
+  return inverse_dynamics<double>(m, batch, q, qd, qdd, tau, stream, &u);
+}
+rd_status_t rd_inverse_dynamics_bnd_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,
+                                        const float* qdd, const float* V0, const float* Vdot0,
+                                        const float* Ftip, float* tau, void* stream) {
+  const UserStateBoundary u{V0, Vdot0, Ftip};
+  return inverse_dynamics<float>(m, batch, q, qd, qdd, tau, stream, &u);
+}
+rd_status_t rd_forward_dynamics_bnd_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                        const double* tau, const double* V0, const double* Vdot0,
+                                        const double* Ftip, double* qdd, int32_t* status, void* stream) {
+  const UserStateBoundary u{V0, Vdot0, Ftip};
+  return forward_dynamics<double>(m, batch, q, qd, tau, qdd, stream, status, &u);
+}
+rd_status_t rd_forward_dynamics_bnd_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,
+                                        const float* tau, const float* V0, const float* Vdot0,
+                                        const float* Ftip, float* qdd, int32_t* status, void* stream) {
+  const UserStateBoundary u{V0, Vdot0, Ftip};
+  return forward_dynamics<float>(m, batch, q, qd, tau, qdd, stream, status, &u);
 }
 rd_status_t rd_forward_dynamics_ex_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
                                        const double* tau, double* qdd, int32_t* status, void* stream) {

@@ -49,6 +49,25 @@ struct Boundary {
   T V0[6], Vd0[6], Ftip[6];
 };
 
+// Per-state boundary data (NEXT-4, rd_*_dynamics_bnd_*): device arrays [6][B]
+// (component-major, x[k*B + b]) in the USER's frames, or nullptr for the
+// model's value; A0 maps a base-frame twist into the kernel's base frame
+// (identity for joint frames, Ad_{D_0^-1} for DH frames), At a wrench in user
+// frame n into the kernel's frame n (Ad_{T_n}^T).
+template <typename T>
+struct StateBoundary {
+  const T* V0;
+  const T* Vd0;
+  const T* Ft;
+  T A0[36];
+  T At[36];
+};
+// Kernel argument type: the full struct for the per-state instantiation, an
+// empty tag otherwise (so the model-boundary kernels keep their parameter list).
+struct NoStateBoundary {};
+template <typename T, bool SB> struct SBArg { typedef NoStateBoundary type; };
+template <typename T> struct SBArg<T, true> { typedef StateBoundary<T> type; };
+
 // Kernel-parameter image for the compile-time-N kernels (lives in the constant
 // bank; every access has a compile-time offset so the DFMAs take it directly).
 template <typename T, int N>
@@ -71,21 +90,25 @@ enum Strategy { kAuto = 0, kThread = 1, kWarpScan = 2, kGeneric = 3 };
 template <typename T>
 cudaError_t launch_rnea_thread(int n, const LinkDH<T>* L_host, const Boundary<T>& bnd,
                                int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
-                               cudaStream_t st, int* launches, bool* supported, uint32_t prism_mask = 0);
+                               cudaStream_t st, int* launches, bool* supported, uint32_t prism_mask = 0,
+                               const StateBoundary<T>* sb = nullptr);
 template <typename T>
 cudaError_t launch_rnea_generic(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                                 int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
-                                T* ws, int64_t ws_slots, cudaStream_t st, int* launches);
+                                T* ws, int64_t ws_slots, cudaStream_t st, int* launches,
+                                const StateBoundary<T>* sb = nullptr);
 // qdd == nullptr: qdd = 0; tau == nullptr: not stored; fhat != nullptr: the
 // per-link bias wrench Fhat (joint frame) is stored as [n][6][B].
 template <typename T>
 cudaError_t launch_rnea_warp(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                              int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
-                             cudaStream_t st, int* launches, bool* supported, T* fhat = nullptr);
+                             cudaStream_t st, int* launches, bool* supported, T* fhat = nullptr,
+                             const StateBoundary<T>* sb = nullptr);
 template <typename T>
 cudaError_t launch_aba(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                        int64_t B, const T* q, const T* qd, const T* tau, T* qdd,
-                       T* ws, int64_t ws_slots, cudaStream_t st, int* launches, int32_t* status);
+                       T* ws, int64_t ws_slots, cudaStream_t st, int* launches, int32_t* status,
+                       const StateBoundary<T>* sb = nullptr);
 
 template <typename T>
 cudaError_t launch_rnea_warp13(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
@@ -103,12 +126,13 @@ cudaError_t launch_rnea_block(int n, const LinkConst<T>* L_dev, const Boundary<T
 template <typename T>
 cudaError_t launch_rnea_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd,
                             int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
-                            cudaStream_t st, int* launches, const unsigned char* prism = nullptr);
+                            cudaStream_t st, int* launches, const unsigned char* prism = nullptr,
+                            const StateBoundary<T>* sb = nullptr);
 template <typename T>
 cudaError_t launch_aba_dh(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd,
                           int64_t B, const T* q, const T* qd, const T* tau, T* qdd,
                           T* ws, int64_t ws_slots, cudaStream_t st, int* launches, int32_t* status,
-                          const unsigned char* prism = nullptr);
+                          const unsigned char* prism = nullptr, const StateBoundary<T>* sb = nullptr);
 template <typename T>
 cudaError_t launch_fd_scan(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                            int64_t B, const T* q, const T* qd, const T* tau, T* qdd, T* ws,

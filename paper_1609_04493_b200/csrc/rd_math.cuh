@@ -291,4 +291,19 @@ __device__ __forceinline__ void dh_link(const LinkDH<T>& C, bool prism, T qi, T*
   *p2 = PR ? fma(C.ca, dq, C.p2) : C.p2;
 }
 
+// Per-state boundary vector of state b: out = A u, u = p[k*B + b] (k = 0..5).
+template <typename T>
+__device__ __forceinline__ void sb_vec(const T* __restrict__ p, const T* A, int64_t B, int64_t b, T* out) {
+  T u[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) u[k] = __ldg(p + (int64_t)k * B + b);
+#pragma unroll
+  for (int r = 0; r < 6; ++r) {
+    T acc = A[6 * r] * u[0];
+#pragma unroll
+    for (int c = 1; c < 6; ++c) acc = fma(A[6 * r + c], u[c], acc);
+    out[r] = acc;
+  }
+}
+
 }  // namespace rd

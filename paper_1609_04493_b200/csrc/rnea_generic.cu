@@ -25,17 +25,22 @@ int64_t generic_ws_slots(int64_t B) {
   return want < max_slots ? want : max_slots;
 }
 
-template <typename T>
+template <typename T, bool SB>
 __global__ void __launch_bounds__(kGenThreads)
 rnea_generic_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int64_t B,
                     const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
-                    T* __restrict__ tau, T* __restrict__ ws, int64_t slots) {
+                    T* __restrict__ tau, T* __restrict__ ws, int64_t slots,
+                    const typename SBArg<T, SB>::type sb) {
   const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= slots) return;
   for (int64_t b = slot; b < B; b += slots) {
     T V[6], Vd[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) { V[k] = bnd.V0[k]; Vd[k] = bnd.Vd0[k]; }
+    if constexpr (SB) {                              // per-state V_0, Vdot_0 (NEXT-4)
+      if (sb.V0) sb_vec(sb.V0, sb.A0, B, b, V);
+      if (sb.Vd0) sb_vec(sb.Vd0, sb.A0, B, b, Vd);
+    }
     for (int i = 0; i < n; ++i) {
       const LinkConst<T> C = L[i];
       const T qi = __ldg(q + (int64_t)i * B + b);
@@ -61,6 +66,9 @@ rnea_generic_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T>
     T F[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) F[k] = bnd.Ftip[k];
+    if constexpr (SB) {
+      if (sb.Ft) sb_vec(sb.Ft, sb.At, B, b, F);
+    }
     bool tip = true;
     Rot<T> Rn;
     T pn0 = 0, pn1 = 0, pn2 = 0;
@@ -93,18 +101,23 @@ rnea_generic_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T>
 template <typename T>
 cudaError_t launch_rnea_generic(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B,
                                 const T* q, const T* qd, const T* qdd, T* tau, T* ws, int64_t ws_slots,
-                                cudaStream_t st, int* launches) {
+                                cudaStream_t st, int* launches, const StateBoundary<T>* sb) {
   const int64_t grid = (ws_slots + kGenThreads - 1) / kGenThreads;
-  rnea_generic_kernel<T><<<(unsigned)grid, kGenThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau, ws, ws_slots);
+  if (sb)
+    rnea_generic_kernel<T, true><<<(unsigned)grid, kGenThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau, ws,
+                                                                          ws_slots, *sb);
+  else
+    rnea_generic_kernel<T, false><<<(unsigned)grid, kGenThreads, 0, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau, ws,
+                                                                           ws_slots, NoStateBoundary{});
   ++*launches;
   return cudaGetLastError();
 }
 
 template cudaError_t launch_rnea_generic<double>(int, const LinkConst<double>*, const Boundary<double>&, int64_t,
                                                  const double*, const double*, const double*, double*, double*,
-                                                 int64_t, cudaStream_t, int*);
+                                                 int64_t, cudaStream_t, int*, const StateBoundary<double>*);
 template cudaError_t launch_rnea_generic<float>(int, const LinkConst<float>*, const Boundary<float>&, int64_t,
                                                 const float*, const float*, const float*, float*, float*,
-                                                int64_t, cudaStream_t, int*);
+                                                int64_t, cudaStream_t, int*, const StateBoundary<float>*);
 
 }  // namespace rd

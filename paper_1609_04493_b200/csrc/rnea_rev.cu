@@ -31,11 +31,12 @@ constexpr int kRevThreads = 128;
 #endif
 constexpr int kRevPD = RD_REV_PD, kRevU = RD_REV_U;
 
-template <typename T, bool PR>
+template <typename T, bool PR, bool SB>
 __global__ void __launch_bounds__(kRevThreads, 4)
 rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
                 const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
-                T* __restrict__ tau, const unsigned char* __restrict__ prism_g) {
+                T* __restrict__ tau, const unsigned char* __restrict__ prism_g,
+                const typename SBArg<T, SB>::type sb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LinkDH<T>* L = reinterpret_cast<LinkDH<T>*>(smem_raw);       // model constants, broadcast reads
   unsigned char* PRs = smem_raw + (size_t)n * sizeof(LinkDH<T>);   // prismatic flags (PR only)
@@ -51,6 +52,10 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
     T V[6], Vd[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) { V[k] = bnd.V0[k]; Vd[k] = bnd.Vd0[k]; }
+    if constexpr (SB) {                              // per-state V_0, Vdot_0 (NEXT-4)
+      if (sb.V0) sb_vec(sb.V0, sb.A0, B, b, V);
+      if (sb.Vd0) sb_vec(sb.Vd0, sb.A0, B, b, Vd);
+    }
     // ---- forward sweep, Eq. (1)
     constexpr int PD = kRevPD;
     T aq[PD], aqd[PD], aqa[PD];
@@ -91,6 +96,9 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
     T F[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) F[k] = bnd.Ftip[k];
+    if constexpr (SB) {
+      if (sb.Ft) sb_vec(sb.Ft, sb.At, B, b, F);
+    }
     T ca = 1, sa = 0, p0 = 0, p1 = 0, p2 = 0, sn = 0, cn = 1;   // child transform (identity at the tip)
 #pragma unroll
     for (int j = 0; j < PD; ++j) {
@@ -138,36 +146,41 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
   }
 }
 
-template <typename T, bool PR>
+template <typename T, bool PR, bool SB>
 static cudaError_t launch_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
-                              const T* qd, const T* qdd, T* tau, cudaStream_t st, const unsigned char* prism) {
+                              const T* qd, const T* qdd, T* tau, cudaStream_t st, const unsigned char* prism,
+                              const typename SBArg<T, SB>::type& sb) {
   const size_t smem = (size_t)n * sizeof(LinkDH<T>) + (PR ? (size_t)n : 0);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(rnea_rev_kernel<T, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(rnea_rev_kernel<T, PR, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
   int64_t grid = (B + kRevThreads - 1) / kRevThreads;
   const int64_t cap = (int64_t)num_sms() * 4;
   if (grid > cap) grid = cap;
-  rnea_rev_kernel<T, PR><<<(unsigned)grid, kRevThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau, prism);
+  rnea_rev_kernel<T, PR, SB><<<(unsigned)grid, kRevThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau, prism,
+                                                                         sb);
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_rnea_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                             const T* qd, const T* qdd, T* tau, cudaStream_t st, int* launches,
-                            const unsigned char* prism) {
+                            const unsigned char* prism, const StateBoundary<T>* sb) {
   ++*launches;
-  return prism ? launch_rev<T, true>(n, L_dev, bnd, B, q, qd, qdd, tau, st, prism)
-               : launch_rev<T, false>(n, L_dev, bnd, B, q, qd, qdd, tau, st, nullptr);
+  if (sb)
+    return prism ? launch_rev<T, true, true>(n, L_dev, bnd, B, q, qd, qdd, tau, st, prism, *sb)
+                 : launch_rev<T, false, true>(n, L_dev, bnd, B, q, qd, qdd, tau, st, nullptr, *sb);
+  return prism ? launch_rev<T, true, false>(n, L_dev, bnd, B, q, qd, qdd, tau, st, prism, NoStateBoundary{})
+               : launch_rev<T, false, false>(n, L_dev, bnd, B, q, qd, qdd, tau, st, nullptr, NoStateBoundary{});
 }
 
 template cudaError_t launch_rnea_rev<double>(int, const LinkDH<double>*, const Boundary<double>&, int64_t,
                                              const double*, const double*, const double*, double*, cudaStream_t,
-                                             int*, const unsigned char*);
+                                             int*, const unsigned char*, const StateBoundary<double>*);
 template cudaError_t launch_rnea_rev<float>(int, const LinkDH<float>*, const Boundary<float>&, int64_t,
                                             const float*, const float*, const float*, float*, cudaStream_t, int*,
-                                            const unsigned char*);
+                                            const unsigned char*, const StateBoundary<float>*);
 
 }  // namespace rd

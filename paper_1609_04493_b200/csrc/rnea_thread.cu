@@ -310,11 +310,11 @@ __device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& 
   g.c = cur[1];
 }
 
-template <typename T, int W, bool PR>
+template <typename T, int W, bool PR, bool SB>
 __global__ void __launch_bounds__(W * 32, 1)
 rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
                       const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
-                      T* __restrict__ tau) {
+                      T* __restrict__ tau, const __grid_constant__ typename SBArg<T, SB>::type sb) {
   constexpr int NT = W * 32;
   constexpr int kColsPerWarp = 2048 / W;
   constexpr int KC = TmemIO<T>::kCols;
@@ -404,6 +404,9 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
       // epilogue: backward of the last tile alone (slot parity of tile it-1)
       const int bpar = (int)((it - 1) & 1);
       bwd_init(g, P);
+      if constexpr (SB) {                            // per-state F_{n+1} of tile it-1 (NEXT-4)
+        if (sb.Ft) sb_vec(sb.Ft, sb.At, B, min(g.b, B - 1), g.F);
+      }
       for (int i = n - 1; i >= 0; --i) {
         T cur[8];
         get_any(bpar ? n - 1 - i : i, cur);
@@ -414,6 +417,10 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
     }
     const int64_t bn = b + (int64_t)gridDim.x * NT;
     fwd_init(f, P, B, fvalid ? b : (B - 1), bn < B ? bn : (B - 1), q, qd, qdd, it == 0 || P.n < Cfg::kPD);
+    if constexpr (SB) {                              // per-state V_0, Vdot_0 (NEXT-4)
+      if (sb.V0) sb_vec(sb.V0, sb.A0, B, fvalid ? b : (B - 1), f.V);
+      if (sb.Vd0) sb_vec(sb.Vd0, sb.A0, B, fvalid ? b : (B - 1), f.Vd);
+    }
     if (it == 0) {
       // prologue: forward of the first tile alone (parity 0: slot = link)
       for (int k = 0; k < n; ++k) {
@@ -425,6 +432,9 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
       // steady state: backward of tile it-1 (parity bpar) + forward of tile it (parity !bpar);
       // at step k both use slot s_k = bpar ? k : n-1-k.
       bwd_init(g, P);
+      if constexpr (SB) {                            // per-state F_{n+1} of tile it-1 (NEXT-4)
+        if (sb.Ft) sb_vec(sb.Ft, sb.At, B, min(g.b, B - 1), g.F);
+      }
       const int bpar = (int)((it - 1) & 1);
       auto smem_step = [&](int k) {
         const int slot = bpar ? k : n - 1 - k;
@@ -513,28 +523,28 @@ bool thread_kernel_has_n(int n, bool fp64) {
   return fp64 ? plan_for<double>(n, &p) : plan_for<float>(n, &p);
 }
 
-template <typename T, int W, bool PR>
+template <typename T, int W, bool PR, bool SB>
 static cudaError_t launch_w(const ThreadParams<T>& P, size_t smem, int64_t B, const T* q, const T* qd,
-                            const T* qdd, T* tau, cudaStream_t st) {
+                            const T* qdd, T* tau, cudaStream_t st, const typename SBArg<T, SB>::type& sb) {
   static thread_local int attr_dev = -1;          // the opt-in is per device; set it once
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(rnea_thread_pp_kernel<T, W, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(rnea_thread_pp_kernel<T, W, PR, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(kSmemCap - 1024));
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
   const int64_t ntiles = (B + W * 32 - 1) / (W * 32);
   const int64_t grid = ntiles < num_sms() ? ntiles : num_sms();
-  rnea_thread_pp_kernel<T, W, PR><<<(unsigned)grid, W * 32, smem, st>>>(P, B, q, qd, qdd, tau);
+  rnea_thread_pp_kernel<T, W, PR, SB><<<(unsigned)grid, W * 32, smem, st>>>(P, B, q, qd, qdd, tau, sb);
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_rnea_thread(int n, const LinkDH<T>* L_host, const Boundary<T>& bnd, int64_t B,
                                const T* q, const T* qd, const T* qdd, T* tau, cudaStream_t st,
-                               int* launches, bool* supported, uint32_t prism_mask) {
+                               int* launches, bool* supported, uint32_t prism_mask, const StateBoundary<T>* sb) {
   StashPlan plan;
   *supported = n >= 1 && n <= kMaxThreadN && plan_for<T>(n, &plan);
   if (!*supported) return cudaSuccess;
@@ -545,19 +555,28 @@ cudaError_t launch_rnea_thread(int n, const LinkDH<T>* L_host, const Boundary<T>
   P.lt = plan.lt;
   ++*launches;
   P.prism = prism_mask;
-  if (prism_mask != 0) {                           // any prismatic joint: the PR instantiation
-    if (plan.W == 16) return launch_w<T, 16, true>(P, plan.smem, B, q, qd, qdd, tau, st);
-    return launch_w<T, 8, true>(P, plan.smem, B, q, qd, qdd, tau, st);
+  const NoStateBoundary nsb{};
+  if (sb) {                                        // per-state boundary: the SB instantiations
+    if (prism_mask != 0) {
+      if (plan.W == 16) return launch_w<T, 16, true, true>(P, plan.smem, B, q, qd, qdd, tau, st, *sb);
+      return launch_w<T, 8, true, true>(P, plan.smem, B, q, qd, qdd, tau, st, *sb);
+    }
+    if (plan.W == 16) return launch_w<T, 16, false, true>(P, plan.smem, B, q, qd, qdd, tau, st, *sb);
+    return launch_w<T, 8, false, true>(P, plan.smem, B, q, qd, qdd, tau, st, *sb);
   }
-  if (plan.W == 16) return launch_w<T, 16, false>(P, plan.smem, B, q, qd, qdd, tau, st);
-  return launch_w<T, 8, false>(P, plan.smem, B, q, qd, qdd, tau, st);
+  if (prism_mask != 0) {                           // any prismatic joint: the PR instantiation
+    if (plan.W == 16) return launch_w<T, 16, true, false>(P, plan.smem, B, q, qd, qdd, tau, st, nsb);
+    return launch_w<T, 8, true, false>(P, plan.smem, B, q, qd, qdd, tau, st, nsb);
+  }
+  if (plan.W == 16) return launch_w<T, 16, false, false>(P, plan.smem, B, q, qd, qdd, tau, st, nsb);
+  return launch_w<T, 8, false, false>(P, plan.smem, B, q, qd, qdd, tau, st, nsb);
 }
 
 template cudaError_t launch_rnea_thread<double>(int, const LinkDH<double>*, const Boundary<double>&, int64_t,
                                                 const double*, const double*, const double*, double*,
-                                                cudaStream_t, int*, bool*, uint32_t);
+                                                cudaStream_t, int*, bool*, uint32_t, const StateBoundary<double>*);
 template cudaError_t launch_rnea_thread<float>(int, const LinkDH<float>*, const Boundary<float>&, int64_t,
                                                const float*, const float*, const float*, float*,
-                                               cudaStream_t, int*, bool*, uint32_t);
+                                               cudaStream_t, int*, bool*, uint32_t, const StateBoundary<float>*);
 
 }  // namespace rd

@@ -29,11 +29,11 @@ __device__ __forceinline__ T shup(T v, int d) { return __shfl_up_sync(0xffffffff
 template <typename T>
 __device__ __forceinline__ T shdn(T v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
 
-template <typename T>
+template <typename T, bool SB>
 __global__ void __launch_bounds__(kWarpCta * 32)
 rnea_warp_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
                  const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
-                 T* __restrict__ tau, T* __restrict__ fhat) {
+                 T* __restrict__ tau, T* __restrict__ fhat, const typename SBArg<T, SB>::type sb) {
   // per-link constants in shared memory, structure-of-arrays [field][32] (lane-contiguous)
   constexpr int NF = sizeof(LinkConst<T>) / sizeof(T);
   __shared__ T sc[NF][32];
@@ -121,8 +121,16 @@ rnea_warp_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> b
         if (lane >= dd) V[k] += o;
       }
     }
+    {
+      T v0[6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) V[k] += bnd.V0[k];
+      for (int k = 0; k < 6; ++k) v0[k] = bnd.V0[k];
+      if constexpr (SB) {                            // per-state V_0 (NEXT-4)
+        if (sb.V0) sb_vec(sb.V0, sb.A0, B, b, v0);
+      }
+#pragma unroll
+      for (int k = 0; k < 6; ++k) V[k] += v0[k];
+    }
     // Vd0 = Vd_0 + prefix sum of S0 qdd + ad_{V0}(S0 qd)
     T A[6];
     {
@@ -144,8 +152,16 @@ rnea_warp_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> b
         if (lane >= dd) A[k] += o;
       }
     }
+    {
+      T a0[6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) A[k] += bnd.Vd0[k];
+      for (int k = 0; k < 6; ++k) a0[k] = bnd.Vd0[k];
+      if constexpr (SB) {
+        if (sb.Vd0) sb_vec(sb.Vd0, sb.A0, B, b, a0);
+      }
+#pragma unroll
+      for (int k = 0; k < 6; ++k) A[k] += a0[k];
+    }
     // body-frame V_l, Vdot_l = Ad_{g^-1}(.), bias wrench Fhat_l, back to the base frame
     T Vb[6], Ab[6], Fh[6];
     ad_finv(R, p0, p1, p2, V, Vb);
@@ -162,9 +178,15 @@ rnea_warp_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> b
 #pragma unroll
       for (int k = 0; k < 6; ++k) F[k] = 0;
     }
+    T ftip[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) ftip[k] = bnd.Ftip[k];
+    if constexpr (SB) {
+      if (sb.Ft) sb_vec(sb.Ft, sb.At, B, b, ftip);
+    }
     if (lane == n - 1) {                             // tip wrench F_{n+1} (frame n) to the base frame
       T Ft[6];
-      bwd_step(R, p0, p1, p2, bnd.Ftip, zero6, Ft);
+      bwd_step(R, p0, p1, p2, ftip, zero6, Ft);
 #pragma unroll
       for (int k = 0; k < 6; ++k) F[k] += Ft[k];
     }
@@ -188,22 +210,27 @@ rnea_warp_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> b
 template <typename T>
 cudaError_t launch_rnea_warp(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                              const T* qd, const T* qdd, T* tau, cudaStream_t st, int* launches,
-                             bool* supported, T* fhat) {
+                             bool* supported, T* fhat, const StateBoundary<T>* sb) {
   *supported = n >= 1 && n <= 32;
   if (!*supported) return cudaSuccess;
   int64_t grid = (B + kWarpCta - 1) / kWarpCta;
   const int64_t cap = (int64_t)num_sms() * 16;
   if (grid > cap) grid = cap;
-  rnea_warp_kernel<T><<<(unsigned)grid, kWarpCta * 32, 0, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau, fhat);
+  if (sb)
+    rnea_warp_kernel<T, true><<<(unsigned)grid, kWarpCta * 32, 0, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau, fhat,
+                                                                         *sb);
+  else
+    rnea_warp_kernel<T, false><<<(unsigned)grid, kWarpCta * 32, 0, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau, fhat,
+                                                                          NoStateBoundary{});
   ++*launches;
   return cudaGetLastError();
 }
 
 template cudaError_t launch_rnea_warp<double>(int, const LinkConst<double>*, const Boundary<double>&, int64_t,
                                               const double*, const double*, const double*, double*, cudaStream_t,
-                                              int*, bool*, double*);
+                                              int*, bool*, double*, const StateBoundary<double>*);
 template cudaError_t launch_rnea_warp<float>(int, const LinkConst<float>*, const Boundary<float>&, int64_t,
                                              const float*, const float*, const float*, float*, cudaStream_t, int*,
-                                             bool*, float*);
+                                             bool*, float*, const StateBoundary<float>*);
 
 }  // namespace rd

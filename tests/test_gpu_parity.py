@@ -238,6 +238,65 @@ def test_full_boundary_V0_Vdot0_Ftip(rd):
         assert rel_err_per_state(tau, ref).max() <= 1e-10
 
 
+def _per_state_boundary(rng, B, which):
+    arrs = [rng.standard_normal((6, B)) if w else None for w in which]
+    return arrs
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("kind", ["revolute", "prismatic", "screw"])
+def test_per_state_boundary_id(rd, dtype, kind):
+    # NEXT-4: V_0, Vdot_0, F_{n+1} per state (rd_inverse_dynamics_bnd_*), every supported strategy
+    n, B = 9, 300
+    r = synth.random_chain(n, 61, prismatic_fraction=0.0 if kind == "revolute" else 0.4)
+    if kind == "screw":
+        i = int(np.argmax(np.linalg.norm(r["S"][:, 3:], axis=1)))
+        r["S"][i, :3] += 0.2 * r["S"][i, 3:]
+    rng = np.random.default_rng(7)
+    q, qd, qdd = synth.states(16, n, 0, B)
+    model = rd.Model.from_robot(r, synth.GRAVITY_Z)
+    for which in ((1, 1, 1), (0, 0, 1), (1, 0, 0)):
+        V0, Vd0, Ft = _per_state_boundary(rng, B, which)
+        gv0, gvd0, gft = oracle.gravity_boundary(synth.GRAVITY_Z)   # the model's values (A3)
+        ref = np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b],
+                                    V0=gv0 if V0 is None else V0[:, b],
+                                    Vd0=gvd0 if Vd0 is None else Vd0[:, b],
+                                    Ftip=gft if Ft is None else Ft[:, b]) for b in range(B)], 1)
+        bnd = tuple(None if a is None else dev(a, dtype) for a in (V0, Vd0, Ft))
+        for strat in ("auto", "thread", "warp_scan", "generic", "reverse"):
+            model.set_strategy(strat)
+            tau = rd.inverse_dynamics(model, dev(q, dtype), dev(qd, dtype), dev(qdd, dtype),
+                                      boundary=bnd).double().cpu().numpy()
+            tol = 1e-10 if dtype == torch.float64 else 2e-4
+            assert rel_err_per_state(tau, ref).max() <= tol, (strat, which)
+    model.set_strategy("warp_scan_eq13")
+    with pytest.raises(rd.RdError):
+        rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd), boundary=(None, None, dev(np.zeros((6, B)))))
+
+
+@pytest.mark.parametrize("kind", ["revolute", "prismatic", "screw"])
+def test_per_state_boundary_fd(rd, kind):
+    n, B = 8, 300
+    r = synth.random_chain(n, 62, prismatic_fraction=0.0 if kind == "revolute" else 0.4)
+    if kind == "screw":
+        i = int(np.argmax(np.linalg.norm(r["S"][:, 3:], axis=1)))
+        r["S"][i, :3] += 0.2 * r["S"][i, 3:]
+    rng = np.random.default_rng(8)
+    q, qd, qdd = synth.states(17, n, 0, B)
+    V0, Vd0, Ft = rng.standard_normal((3, 6, B))
+    tau = np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b], V0[:, b], Vd0[:, b], Ft[:, b])
+                    for b in range(B)], 1)
+    model = rd.Model.from_robot(r, synth.GRAVITY_Z)
+    st = torch.empty(B, dtype=torch.int32, device="cuda")
+    out = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau), status=st,
+                              boundary=(dev(V0), dev(Vd0), dev(Ft))).cpu().numpy()
+    assert rel_err_per_state(out, qdd, floor=1.0).max() < 1e-9
+    assert int(st.abs().max()) == 0
+    model.set_fd_algo("jsiia")
+    with pytest.raises(rd.RdError):
+        rd.forward_dynamics(model, dev(q), dev(qd), dev(tau), boundary=(dev(V0), None, None))
+
+
 def test_deterministic_and_strategy_consistent(rd):
     cfg = synth.CONFIGS["C3"]
     q, qd, qdd = synth.states(cfg["seed"], 30, 0, 20000)

@@ -24,6 +24,13 @@ for dt in (torch.float64, torch.float32):
                 model.set_strategy(strat)
                 rd.inverse_dynamics(model, q, qd, qdd)
             tau = rd.inverse_dynamics(model, q, qd, qdd)
+            bnd = tuple(torch.ones((6, B), dtype=dt, device="cuda") * 0.1 for _ in range(3))
+            for strat in ("thread", "warp_scan", "generic", "reverse"):
+                model.set_strategy(strat)
+                rd.inverse_dynamics(model, q, qd, qdd, boundary=bnd)
+            model.set_strategy("auto")
+            model.set_fd_algo("aba")
+            rd.forward_dynamics(model, q, qd, tau, boundary=bnd)
             for algo in ("aba", "jsiia", "aba_scan", "aba_merged"):
                 if (algo in ("jsiia", "aba_merged") and n > 31) or (algo == "aba_scan" and n > 32):
                     continue
