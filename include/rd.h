@@ -77,7 +77,8 @@ typedef enum {
                              (one per lane of a warp) + Cholesky solve; n <= 31, else RD_E_UNSUPPORTED */
   RD_FD_ABA_SCAN = 2,     /* the paper's hybrid ABIA, Alg. 3, all on the GPU: tau_bias by the warp-scan
                              ID, serial ABI (Eq. 7) per state, then the Eq. (18) zhat and Eq. (19)
-                             lambda scans across the links of a warp; n <= 32 */
+                             lambda scans across the links of a warp (n <= 32) or of a CTA
+                             (32 < n <= 256, warp scans + a scan of the warp totals) */
   RD_FD_ABA_MERGED = 3    /* as RD_FD_ABA_SCAN, but tau_hat, zhat and chat come from ONE backward scan
                              of the merged Eq. (20) operators (Omega^{-1} reading A7,
                              seeding A8) over the n+1 lanes of a warp; n <= 31 */

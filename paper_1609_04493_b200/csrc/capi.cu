@@ -583,7 +583,7 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
         : rd::launch_fd_scan<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
                                 reinterpret_cast<T*>(m->ws), s, &g_launches, &ok, status);
     if (!ok) return fail(RD_E_UNSUPPORTED, merged ? "merged-scan ABIA forward dynamics supports n <= 31 (use RD_FD_ABA)"
-                                                  : "scan-ABIA forward dynamics supports n <= 32 (use RD_FD_ABA)");
+                                                  : "scan-ABIA forward dynamics supports n <= 256 (use RD_FD_ABA)");
     if (e != cudaSuccess) return cuda_fail(e, "forward dynamics (scan ABIA) launch");
     return RD_OK;
   }

@@ -421,16 +421,167 @@ fd_merged_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> b
   }
 }
 
+// ---------------------------------------------------------------- CTA-wide variant (32 < n <= 256)
+// Alg. 3 lines 2, 5-8 for long chains (the paper's fd_200 experiment):
+// one CTA per state, thread = link, the same affine-map scans as fd_scan_kernel
+// done CTA-wide: Kogge-Stone inside each warp (shuffles), the warp totals scanned
+// by warp 0 (shuffles again), then every lane composes with the combined total
+// of the warps after it (suffix scan, Eq. 18) or before it (prefix scan, Eq. 19).
+// Composition is not commutative: the own operator always stays on the left.
+constexpr int kFdBlockMaxN = 256;
+
+// (L, b) := (L, b) o (L2, b2) with (L2, b2) in shared memory
+template <typename T>
+__device__ __forceinline__ void compose_mem(T (&Lm)[36], T (&bv)[6], const T* __restrict__ L2,
+                                            const T* __restrict__ b2) {
+  T nL[36], nb[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    nb[i] = bv[i];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) nL[6 * i + j] = 0;
+  }
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const T bk = b2[k];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const T lik = Lm[6 * i + k];
+#pragma unroll
+      for (int j = 0; j < 6; ++j) nL[6 * i + j] = fma(lik, L2[6 * k + j], nL[6 * i + j]);
+      nb[i] = fma(lik, bk, nb[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 36; ++i) Lm[i] = nL[i];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) bv[i] = nb[i];
+}
+
+// CTA-wide inclusive scan of affine maps; SUFFIX: M_l = A_l o A_{l+1} o ... ,
+// else prefix M_l = A_l o A_{l-1} o ...  (sh: >= 2 * nwarps * 42 scalars)
+template <typename T, bool SUFFIX>
+__device__ __forceinline__ void block_affine_scan(T (&Lm)[36], T (&bv)[6], T* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll 1
+  for (int d = 1; d < 32; d <<= 1)
+    compose_shfl<T, SUFFIX>(Lm, bv, d, SUFFIX ? (lane + d < 32) : (lane >= d));
+  // warp totals: the composite of the whole warp sits on lane 0 (suffix) / lane 31 (prefix)
+  T* tot = sh;                     // [nw][42]
+  if (lane == (SUFFIX ? 0 : 31)) {
+    for (int i = 0; i < 36; ++i) tot[warp * 42 + i] = Lm[i];
+    for (int i = 0; i < 6; ++i) tot[warp * 42 + 36 + i] = bv[i];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    T TL[36], Tb[6];
+    if (lane < nw) {
+      for (int i = 0; i < 36; ++i) TL[i] = tot[lane * 42 + i];
+      for (int i = 0; i < 6; ++i) Tb[i] = tot[lane * 42 + 36 + i];
+    } else {
+      for (int i = 0; i < 36; ++i) TL[i] = (i % 7 == 0) ? T(1) : T(0);
+      for (int i = 0; i < 6; ++i) Tb[i] = 0;
+    }
+#pragma unroll 1
+    for (int d = 1; d < 32; d <<= 1)
+      compose_shfl<T, SUFFIX>(TL, Tb, d, SUFFIX ? (lane + d < 32) : (lane >= d));
+    T* acc = sh + nw * 42;         // [nw][42]: combined totals
+    if (lane < nw) {
+      for (int i = 0; i < 36; ++i) acc[lane * 42 + i] = TL[i];
+      for (int i = 0; i < 6; ++i) acc[lane * 42 + 36 + i] = Tb[i];
+    }
+  }
+  __syncthreads();
+  const int src = SUFFIX ? warp + 1 : warp - 1;
+  if (src >= 0 && src < nw) {
+    const T* acc = sh + nw * 42 + src * 42;
+    compose_mem(Lm, bv, acc, acc + 36);
+  }
+  __syncthreads();                 // sh is reused by the caller
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kFdBlockMaxN)
+fd_scan_block_kernel(int n, const LinkConst<T>* __restrict__ Lg, int64_t B, const T* __restrict__ q,
+                     const T* __restrict__ tau_in, const T* __restrict__ tau_bias, const T* __restrict__ pi_ws,
+                     T* __restrict__ qdd_out) {
+  __shared__ T sh[2 * (kFdBlockMaxN / 32) * 42];
+  __shared__ T edge[(kFdBlockMaxN / 32) * 6];
+  const int l = threadIdx.x, lane = l & 31, warp = l >> 5, nw = blockDim.x >> 5;
+  const bool act = l < n;
+  LinkConst<T> C;
+  if (act) C = Lg[l];
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    T Y[36], zb[6], Pi[6], D = 1, th = 0, al = 0, be = 0;
+    Rot<T> R;
+    T p0, p1, p2;
+    scan_link_setup(act, C, n, B, b, l, q, pi_ws, Y, Pi, D, R, p0, p1, p2);
+    if (act) {
+      th = __ldg(tau_in + (int64_t)l * B + b) - __ldg(tau_bias + (int64_t)l * B + b);   // line 2
+      al = C.alpha;
+      be = C.beta;
+    }
+#pragma unroll
+    for (int i = 0; i < 6; ++i) zb[i] = Pi[i] * th;
+    // line 5: suffix scan of z -> Y z + Pi tau_hat
+    T Lm[36];
+#pragma unroll
+    for (int i = 0; i < 36; ++i) Lm[i] = Y[i];
+    block_affine_scan<T, true>(Lm, zb, sh);
+    // zhat_l = offset of the composite starting at l + 1 (lane 31: the next warp's lane 0)
+    if (lane == 0)
+      for (int k = 0; k < 6; ++k) edge[warp * 6 + k] = zb[k];
+    __syncthreads();
+    T z[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const T o = __shfl_down_sync(0xffffffffu, zb[k], 1);
+      const T e = (lane == 31 && warp + 1 < nw) ? edge[(warp + 1) * 6 + k] : o;
+      z[k] = (l + 1 < n) ? e : T(0);
+    }
+    __syncthreads();
+    // line 6
+    const T ch = (th - fma(be, z[2], al * z[5])) / D;
+    // line 7: prefix scan of lam -> Y^T lam + S chat
+    T lb[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int j = 0; j < 6; ++j) Lm[6 * i + j] = Y[6 * j + i];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) lb[k] = 0;
+    lb[2] = be * ch;
+    lb[5] = al * ch;
+    block_affine_scan<T, false>(Lm, lb, sh);
+    // line 8: qdd_l = chat_l - Pi_l^T lam_{l-1} (lane 0: the previous warp's lane 31)
+    if (lane == 31)
+      for (int k = 0; k < 6; ++k) edge[warp * 6 + k] = lb[k];
+    __syncthreads();
+    T acc = 0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const T o = __shfl_up_sync(0xffffffffu, lb[k], 1);
+      const T e = (lane == 0 && warp > 0) ? edge[(warp - 1) * 6 + k] : o;
+      acc = fma(Pi[k], l > 0 ? e : T(0), acc);
+    }
+    __syncthreads();
+    if (act) qdd_out[(int64_t)l * B + b] = ch - acc;
+  }
+}
+
 template <typename T>
 cudaError_t launch_fd_scan(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                            const T* qd, const T* tau, T* qdd, T* ws, cudaStream_t st, int* launches,
                            bool* supported, int32_t* status) {
-  *supported = n >= 1 && n <= 32;
+  *supported = n >= 1 && n <= kFdBlockMaxN;
   if (!*supported) return cudaSuccess;
   T* tau_bias = ws;                                  // [n][B]
   T* pi_ws = ws + (size_t)n * B;                     // [n][7][B]
   bool ok = false;
-  cudaError_t e = launch_rnea_warp<T>(n, L_dev, bnd, B, q, qd, nullptr, tau_bias, st, launches, &ok);   // line 1
+  const bool block = n > 32;                         // CTA-wide scans for long chains
+  cudaError_t e = block
+      ? launch_rnea_block<T>(n, L_dev, bnd, B, q, qd, nullptr, tau_bias, st, launches, &ok)     // line 1
+      : launch_rnea_warp<T>(n, L_dev, bnd, B, q, qd, nullptr, tau_bias, st, launches, &ok);
   if (e != cudaSuccess) return e;
   int64_t g1 = (B + kAbiThreads - 1) / kAbiThreads;
   if (g1 > (int64_t)num_sms() * 8) g1 = (int64_t)num_sms() * 8;
@@ -438,9 +589,15 @@ cudaError_t launch_fd_scan(int n, const LinkConst<T>* L_dev, const Boundary<T>& 
   ++*launches;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  int64_t g2 = (B + kScanWarps - 1) / kScanWarps;
-  if (g2 > (int64_t)num_sms() * 16) g2 = (int64_t)num_sms() * 16;
-  fd_scan_kernel<T><<<(unsigned)g2, kScanWarps * 32, 0, st>>>(n, L_dev, B, q, tau, tau_bias, pi_ws, qdd);  // 2, 5-8
+  if (block) {
+    int64_t g2 = B < (int64_t)num_sms() * 8 ? B : (int64_t)num_sms() * 8;
+    fd_scan_block_kernel<T><<<(unsigned)g2, ((n + 31) / 32) * 32, 0, st>>>(n, L_dev, B, q, tau, tau_bias, pi_ws,
+                                                                            qdd);
+  } else {
+    int64_t g2 = (B + kScanWarps - 1) / kScanWarps;
+    if (g2 > (int64_t)num_sms() * 16) g2 = (int64_t)num_sms() * 16;
+    fd_scan_kernel<T><<<(unsigned)g2, kScanWarps * 32, 0, st>>>(n, L_dev, B, q, tau, tau_bias, pi_ws, qdd);  // 2, 5-8
+  }
   ++*launches;
   return cudaGetLastError();
 }

@@ -149,7 +149,7 @@ rnea_block_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> 
     if (act) {
       qi = __ldg(q + (int64_t)l * B + b);
       qdi = __ldg(qd + (int64_t)l * B + b);
-      qddi = __ldg(qdd + (int64_t)l * B + b);
+      qddi = qdd ? __ldg(qdd + (int64_t)l * B + b) : T(0);   // qdd == nullptr: tau_bias (Eq. 5)
     }
     // CalcTransform, then the SE(3) scan g_{0,l}
     T s, cc;

@@ -484,7 +484,8 @@ def test_fd_jsiia_boundary_and_limits(rd):
 
 
 # ------------------------------------------------------------------ forward dynamics (scan ABIA, Alg. 3)
-@pytest.mark.parametrize("n,pf", [(1, 0.0), (2, 0.0), (7, 0.3), (16, 0.0), (30, 0.0), (32, 0.2)])
+@pytest.mark.parametrize("n,pf", [(1, 0.0), (2, 0.0), (7, 0.3), (16, 0.0), (30, 0.0), (32, 0.2), (33, 0.0),
+                                  (64, 0.2), (100, 0.0), (200, 0.0), (256, 0.1)])
 def test_fd_aba_scan_parity(rd, n, pf):
     r = synth.random_chain(n, 800 + n, prismatic_fraction=pf)
     g = synth.GRAVITY_Z
@@ -497,7 +498,8 @@ def test_fd_aba_scan_parity(rd, n, pf):
     back = oracle.rnea_batch(r, g, q, qd, out)
     assert rel_err_per_state(back, tau).max() <= 1e-10
     ref = oracle.fd_batch(r, g, q, qd, tau)
-    assert rel_err_per_state(out, ref, floor=1.0).max() < 1e-7
+    # forward error is cond(M)-limited (A14): cond grows fast with n
+    assert rel_err_per_state(out, ref, floor=1.0).max() < (1e-7 if n <= 32 else 1e-5)
     assert rd.last_launch_count() == 3
 
 
@@ -536,9 +538,10 @@ def test_fd_scan_variants_boundary_fp32_limits(rd, algo):
     out32 = rd.forward_dynamics(model, dev(q, torch.float32), dev(qd, torch.float32),
                                 dev(tau, torch.float32)).cpu().numpy()
     assert rel_err_per_state(out32, qdd, floor=1.0).max() < 1e-3
-    big = rd.Model.from_robot(synth.random_chain(33, 1), synth.GRAVITY_Z)
+    nbig = 257 if algo == "aba_scan" else 32                 # beyond the CTA / warp limits
+    big = rd.Model.from_robot(synth.random_chain(nbig, 1), synth.GRAVITY_Z)
     big.set_fd_algo(algo)
-    z = torch.zeros((33, 10), dtype=torch.float64, device="cuda")
+    z = torch.zeros((nbig, 10), dtype=torch.float64, device="cuda")
     with pytest.raises(rd.RdError):
         rd.forward_dynamics(big, z, z, z)
 
