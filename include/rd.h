@@ -74,7 +74,8 @@ typedef enum {
 typedef enum {
   RD_FD_ABA = 0,          /* articulated-body algorithm, Eq. (7)-(8), Alg. 3 (default) */
   RD_FD_JSIIA = 1,        /* joint-space inertia inversion, Eq. (6)/(17), Alg. 2: n+1 IDs per state
-                             (one per lane of a warp) + Cholesky solve; n <= 31, else RD_E_UNSUPPORTED */
+                             (one per lane of a warp, n <= 31, or per thread of a CTA, n <= 256) +
+                             Cholesky solve; n > 256 -> RD_E_UNSUPPORTED */
   RD_FD_ABA_SCAN = 2,     /* the paper's hybrid ABIA, Alg. 3, all on the GPU: tau_bias by the warp-scan
                              ID, serial ABI (Eq. 7) per state, then the Eq. (18) zhat and Eq. (19)
                              lambda scans across the links of a warp (n <= 32) or of a CTA

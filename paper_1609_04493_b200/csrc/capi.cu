@@ -564,10 +564,18 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     make_state_boundary<T>(m, *usb, true, &sbd);
   }
   if (m->fd_algo == RD_FD_JSIIA) {
+    std::unique_lock<std::mutex> lk(m->mu, std::defer_lock);
+    T* jws = nullptr;
+    if (m->n > 31) {                                  // CTA-wide JSIIA: per-CTA M in the model workspace
+      lk.lock();
+      st = ensure_ws(m, rd::jsiia_ws_elems(m->n, batch) * sizeof(T));
+      if (st != RD_OK) return st;
+      jws = reinterpret_cast<T*>(m->ws);
+    }
     bool ok = false;
     cudaError_t e = rd::launch_jsiia<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd, s,
-                                        &g_launches, &ok, status);
-    if (!ok) return fail(RD_E_UNSUPPORTED, "JSIIA forward dynamics supports n <= 31 (use RD_FD_ABA)");
+                                        &g_launches, &ok, status, jws);
+    if (!ok) return fail(RD_E_UNSUPPORTED, "JSIIA forward dynamics supports n <= 256 (use RD_FD_ABA)");
     if (e != cudaSuccess) return cuda_fail(e, "forward dynamics (JSIIA) launch");
     return RD_OK;
   }

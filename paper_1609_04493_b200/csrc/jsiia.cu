@@ -175,12 +175,172 @@ jsiia_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> bnd, 
   }
 }
 
+// ---------------------------------------------------------------- CTA-wide variant (31 < n <= 256)
+// The paper's fd_200 comparison: one CTA per state, thread j < n
+// computes column j of M(q) (Eq. 17), thread n tau_bias (Eq. 5), each with the
+// same stash-free register RNEA as the warp kernel; M (n x n, plus tau_bias in
+// column n) lives in a per-CTA global workspace (L1/L2-resident), factorised by
+// a right-looking Cholesky with one barrier per column (rows of the trailing
+// update spread over the threads), then the two triangular solves with one
+// barrier per step.  O(n^3) per state: the cost the paper attributes to JSIIA
+// at large n.
+constexpr int kJsBlockMaxN = 256;
+constexpr int kJsBlockThreads = 288;      // >= n + 1, whole warps
+
+template <typename T, bool SMEM>
+__global__ void __launch_bounds__(kJsBlockThreads)
+jsiia_block_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
+                   const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ tau_in,
+                   T* __restrict__ qdd_out, int32_t* __restrict__ status, T* __restrict__ ws) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ T strf[3][kJsBlockMaxN];
+  __shared__ T rhs[kJsBlockMaxN];
+  __shared__ T s_piv;
+  __shared__ int s_fail;
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int ld = n + 1;                                    // row stride of M (column n = tau_bias)
+  // M in shared memory when it fits (n <= 160 fp64), else a per-CTA global workspace
+  T* M = SMEM ? reinterpret_cast<T*>(smem_raw) : ws + (size_t)blockIdx.x * (size_t)n * ld;
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    for (int l = t; l < n; l += nt) {                      // CalcTransform, link l
+      const T ql = __ldg(q + (int64_t)l * B + b);
+      T s, c;
+      rd_sincos(Lg[l].alpha * ql, &s, &c);
+      strf[0][l] = s;
+      strf[1][l] = c;
+      strf[2][l] = Lg[l].beta * ql;
+    }
+    __syncthreads();
+    if (t <= n) {
+      const bool bias = t == n;
+      T V[6], Vd[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) { V[k] = bias ? bnd.V0[k] : T(0); Vd[k] = bias ? bnd.Vd0[k] : T(0); }
+      for (int i = 0; i < n; ++i) {
+        const LinkConst<T> C = Lg[i];
+        const T s = strf[0][i], c = strf[1][i], d = strf[2][i];
+        const Rot<T> R = make_rot(C, s, c);
+        const T p0 = fma(d, C.Rm[2], C.pm[0]), p1 = fma(d, C.Rm[5], C.pm[1]), p2 = fma(d, C.Rm[8], C.pm[2]);
+        const T qdi = bias ? __ldg(qd + (int64_t)i * B + b) : T(0);
+        const T qddi = (t == i) ? T(1) : T(0);
+        T Vn[6], Vdn[6];
+        fwd_step<T, false>(C, R, p0, p1, p2, qdi, qddi, V, Vd, Vn, Vdn);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) { V[k] = Vn[k]; Vd[k] = Vdn[k]; }
+      }
+      T F[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) F[k] = bias ? bnd.Ftip[k] : T(0);
+      Rot<T> Rn{1, 0, 0, 0, 1, 0, 0, 0, 1};
+      T pn0 = 0, pn1 = 0, pn2 = 0;
+      for (int i = n - 1; i >= 0; --i) {
+        const LinkConst<T> C = Lg[i];
+        T Fh[6], Fo[6];
+        bias_force(C, V, Vd, Fh);
+        bwd_step(Rn, pn0, pn1, pn2, F, Fh, Fo);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) F[k] = Fo[k];
+        M[(size_t)i * ld + t] = fma(C.beta, F[2], C.alpha * F[5]);   // column t (t = n: tau_bias)
+        const T s = strf[0][i], c = strf[1][i], d = strf[2][i];
+        Rn = make_rot(C, s, c);
+        pn0 = fma(d, C.Rm[2], C.pm[0]); pn1 = fma(d, C.Rm[5], C.pm[1]); pn2 = fma(d, C.Rm[8], C.pm[2]);
+        const T qdi = bias ? __ldg(qd + (int64_t)i * B + b) : T(0);
+        const T qddi = (t == i) ? T(1) : T(0);
+        const T a = C.alpha, be = C.beta, aq = a * qdi, bq = be * qdi;
+        T x[6], y[6];
+        y[0] = Vd[0] - fma(bq, V[4], aq * V[1]);
+        y[1] = Vd[1] + fma(bq, V[3], aq * V[0]);
+        y[2] = Vd[2] - be * qddi;
+        y[3] = Vd[3] - aq * V[4];
+        y[4] = Vd[4] + aq * V[3];
+        y[5] = Vd[5] - a * qddi;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) x[k] = V[k];
+        x[2] -= bq;
+        x[5] -= aq;
+        ad_f(Rn, pn0, pn1, pn2, x, V);
+        ad_f(Rn, pn0, pn1, pn2, y, Vd);
+      }
+    }
+    if (t == 0) s_fail = 0;
+    __syncthreads();
+    for (int i = t; i < n; i += nt) rhs[i] = __ldg(tau_in + (int64_t)i * B + b) - M[(size_t)i * ld + n];   // line 2
+    // Cholesky M = L L^T, lower triangle in place
+    for (int k = 0; k < n; ++k) {
+      if (t == 0) {
+        const T piv = M[(size_t)k * ld + k];
+        if (s_fail == 0 && !(piv > T(0))) s_fail = k + 1;
+        const T lkk = sqrt(piv > T(0) ? piv : T(1));
+        M[(size_t)k * ld + k] = lkk;
+        s_piv = lkk;
+      }
+      __syncthreads();
+      const T inv = T(1) / s_piv;
+      for (int i = k + 1 + t; i < n; i += nt) M[(size_t)i * ld + k] *= inv;
+      __syncthreads();
+      for (int i = k + 1 + t; i < n; i += nt) {
+        const T lik = M[(size_t)i * ld + k];
+        for (int j = k + 1; j <= i; ++j) M[(size_t)i * ld + j] = fma(-lik, M[(size_t)j * ld + k], M[(size_t)i * ld + j]);
+      }
+      __syncthreads();
+    }
+    // L y = rhs, then L^T x = y (column sweeps)
+    for (int i = 0; i < n; ++i) {
+      const T yi = rhs[i] / M[(size_t)i * ld + i];
+      __syncthreads();
+      for (int j = i + 1 + t; j < n; j += nt) rhs[j] = fma(-M[(size_t)j * ld + i], yi, rhs[j]);
+      if (t == 0) rhs[i] = yi;
+      __syncthreads();
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      const T xi = rhs[i] / M[(size_t)i * ld + i];
+      __syncthreads();
+      for (int j = t; j < i; j += nt) rhs[j] = fma(-M[(size_t)i * ld + j], xi, rhs[j]);
+      if (t == 0) rhs[i] = xi;
+      __syncthreads();
+    }
+    const bool spd = s_fail == 0;
+    for (int i = t; i < n; i += nt) qdd_out[(int64_t)i * B + b] = spd ? rhs[i] : T(NAN);
+    if (status && t == 0) status[b] = s_fail;
+    __syncthreads();
+  }
+}
+
+constexpr size_t kJsSmemMax = 200 * 1024;   // + ~9 KB static: one CTA per SM
+int64_t jsiia_block_grid(int64_t B) { return B < (int64_t)num_sms() * 2 ? B : (int64_t)num_sms() * 2; }
+size_t jsiia_ws_elems(int n, int64_t B) {
+  return n > 31 ? (size_t)jsiia_block_grid(B) * (size_t)n * (size_t)(n + 1) : 0;
+}
+
 template <typename T>
 cudaError_t launch_jsiia(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                          const T* qd, const T* tau, T* qdd, cudaStream_t st, int* launches, bool* supported,
-                         int32_t* status) {
-  *supported = n >= 1 && n <= 31;
+                         int32_t* status, T* ws) {
+  *supported = n >= 1 && n <= kJsBlockMaxN;
   if (!*supported) return cudaSuccess;
+  if (n > 31) {
+    const int threads = ((n + 1 + 31) / 32) * 32;
+    const size_t mbytes = (size_t)n * (n + 1) * sizeof(T);
+    ++*launches;
+    if (mbytes <= kJsSmemMax) {
+      static thread_local int attr_dev = -1;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (attr_dev != dev) {
+        cudaError_t e = cudaFuncSetAttribute(jsiia_block_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kJsSmemMax);
+        if (e != cudaSuccess) return e;
+        attr_dev = dev;
+      }
+      const int64_t grid = B < (int64_t)num_sms() ? B : (int64_t)num_sms();
+      jsiia_block_kernel<T, true><<<(unsigned)grid, threads, mbytes, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd,
+                                                                           status, ws);
+    } else {
+      jsiia_block_kernel<T, false><<<(unsigned)jsiia_block_grid(B), threads, 0, st>>>(n, L_dev, bnd, B, q, qd, tau,
+                                                                                      qdd, status, ws);
+    }
+    return cudaGetLastError();
+  }
   int64_t grid = (B + kJsWarps - 1) / kJsWarps;
   const int64_t cap = (int64_t)num_sms() * 16;
   if (grid > cap) grid = cap;
@@ -191,9 +351,9 @@ cudaError_t launch_jsiia(int n, const LinkConst<T>* L_dev, const Boundary<T>& bn
 
 template cudaError_t launch_jsiia<double>(int, const LinkConst<double>*, const Boundary<double>&, int64_t,
                                           const double*, const double*, const double*, double*, cudaStream_t,
-                                          int*, bool*, int32_t*);
+                                          int*, bool*, int32_t*, double*);
 template cudaError_t launch_jsiia<float>(int, const LinkConst<float>*, const Boundary<float>&, int64_t,
                                          const float*, const float*, const float*, float*, cudaStream_t, int*,
-                                         bool*, int32_t*);
+                                         bool*, int32_t*, float*);
 
 }  // namespace rd

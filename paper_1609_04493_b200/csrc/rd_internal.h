@@ -145,7 +145,8 @@ size_t fd_scan_ws_elems(int n, int64_t B);     // workspace (elements) of either
 template <typename T>
 cudaError_t launch_jsiia(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                          int64_t B, const T* q, const T* qd, const T* tau, T* qdd,
-                         cudaStream_t st, int* launches, bool* supported, int32_t* status);
+                         cudaStream_t st, int* launches, bool* supported, int32_t* status, T* ws);
+size_t jsiia_ws_elems(int n, int64_t B);   // workspace of the CTA-wide JSIIA (n > 31), elements
 
 // Workspace slots (threads) the generic / ABA kernels use: ws holds
 // per-link doubles for each slot (see the .cu files for the layout).

@@ -449,7 +449,8 @@ def test_thread_kernel_many_tiles(rd):
 
 
 # ------------------------------------------------------------------ forward dynamics (JSIIA, NEXT-1)
-@pytest.mark.parametrize("n,pf", [(1, 0.0), (2, 0.0), (7, 0.3), (10, 0.0), (30, 0.0), (31, 0.2)])
+@pytest.mark.parametrize("n,pf", [(1, 0.0), (2, 0.0), (7, 0.3), (10, 0.0), (30, 0.0), (31, 0.2), (32, 0.0),
+                                  (64, 0.2), (100, 0.0), (200, 0.0)])
 def test_fd_jsiia_parity(rd, n, pf):
     r = synth.random_chain(n, 700 + n, prismatic_fraction=pf)
     g = synth.GRAVITY_Z
@@ -462,7 +463,7 @@ def test_fd_jsiia_parity(rd, n, pf):
     back = oracle.rnea_batch(r, g, q, qd, out)
     assert rel_err_per_state(back, tau).max() <= 1e-10
     ref = oracle.fd_batch(r, g, q, qd, tau, algo="jsiia")
-    assert rel_err_per_state(out, ref, floor=1.0).max() < 1e-7
+    assert rel_err_per_state(out, ref, floor=1.0).max() < (1e-7 if n <= 31 else 1e-5)   # cond(M), A14
 
 
 def test_fd_jsiia_boundary_and_limits(rd):
@@ -476,9 +477,9 @@ def test_fd_jsiia_boundary_and_limits(rd):
     tau = np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b], V0, Vd0, Ft) for b in range(300)], 1)
     out = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()
     assert rel_err_per_state(out, qdd, floor=1.0).max() < 1e-9
-    big = rd.Model.from_robot(synth.random_chain(40, 1), synth.GRAVITY_Z)
+    big = rd.Model.from_robot(synth.random_chain(257, 1), synth.GRAVITY_Z)
     big.set_fd_algo("jsiia")
-    z = torch.zeros((40, 10), dtype=torch.float64, device="cuda")
+    z = torch.zeros((257, 10), dtype=torch.float64, device="cuda")
     with pytest.raises(rd.RdError):
         rd.forward_dynamics(big, z, z, z)
 

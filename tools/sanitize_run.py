@@ -32,7 +32,7 @@ for dt in (torch.float64, torch.float32):
             model.set_fd_algo("aba")
             rd.forward_dynamics(model, q, qd, tau, boundary=bnd)
             for algo in ("aba", "jsiia", "aba_scan", "aba_merged"):
-                if (algo in ("jsiia", "aba_merged") and n > 31) or (algo == "aba_scan" and n > 256):
+                if (algo == "aba_merged" and n > 31) or (algo in ("jsiia", "aba_scan") and n > 256):
                     continue
                 model.set_fd_algo(algo)
                 rd.forward_dynamics(model, q, qd, tau)
