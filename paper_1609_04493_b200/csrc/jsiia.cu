@@ -278,9 +278,12 @@ jsiia_block_kernel(int n, const LinkConst<T>* __restrict__ Lg, const Boundary<T>
       const T inv = T(1) / s_piv;
       for (int i = k + 1 + t; i < n; i += nt) M[(size_t)i * ld + k] *= inv;
       __syncthreads();
-      for (int i = k + 1 + t; i < n; i += nt) {
-        const T lik = M[(size_t)i * ld + k];
-        for (int j = k + 1; j <= i; ++j) M[(size_t)i * ld + j] = fma(-lik, M[(size_t)j * ld + k], M[(size_t)i * ld + j]);
+      // trailing update, one column j per thread: at each row i the threads of a
+      // warp touch consecutive M[i][j] (coalesced / conflict-free) and share M[i][k]
+      for (int j = k + 1 + t; j < n; j += nt) {
+        const T ljk = M[(size_t)j * ld + k];
+#pragma unroll 4
+        for (int i = j; i < n; ++i) M[(size_t)i * ld + j] = fma(-M[(size_t)i * ld + k], ljk, M[(size_t)i * ld + j]);
       }
       __syncthreads();
     }
