@@ -160,9 +160,9 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle
-    cfg = dict(synth.CONFIGS[args.config], name=args.config)
+    cfg = config_of(args)
     n = cfg["n"]
-    robot = synth.robot_for(cfg)
+    robot = robot_of(cfg)
     g = cfg["gravity"]
     cores = os.cpu_count() or 1
     # bounded sample per step: calibrate the oracle's rate, then size each step so the
@@ -194,7 +194,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{args.config}: n={n} {'FD (ABA)' if fd else 'RNEA'} (bounded sample of {sample} "
+        "config": {"workload": f"{cfg['name']}: n={n} {'FD (ABA)' if fd else 'RNEA'} (bounded sample of {sample} "
                                f"states/step of the workload)",
                    "n": n, "states_per_step": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
@@ -203,6 +203,25 @@ def run_reference(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def config_of(args) -> dict:
+    """The BASELINE config, optionally overridden by --n / --seed / --model (then
+    config.workload says so: the bench line is no longer the config's)."""
+    cfg = dict(synth.CONFIGS[args.config], name=args.config)
+    if args.n:
+        cfg.update(n=args.n, robot="random", name=f"{args.config}+n={args.n}")
+    if args.seed is not None:
+        cfg.update(seed=args.seed, name=cfg["name"] + f"+seed={args.seed}")
+    if args.model:
+        from paper_1609_04493_b200 import model_io
+        cfg.update(model=model_io.load_model(args.model), name=cfg["name"] + f"+model={os.path.basename(args.model)}")
+        cfg["n"] = cfg["model"]["S"].shape[0]
+    return cfg
+
+
+def robot_of(cfg: dict) -> dict:
+    return cfg["model"] if "model" in cfg else synth.robot_for(cfg)
 
 
 def main():
@@ -215,6 +234,9 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--strategy", default="auto")
     ap.add_argument("--batch", type=int, default=0, help="states per GPU (default: the config's)")
+    ap.add_argument("--n", type=int, default=0, help="links of the random chain (overrides the config's n)")
+    ap.add_argument("--seed", type=int, default=None, help="state seed (overrides the config's)")
+    ap.add_argument("--model", default=None, help="robot model file (JSON, paper_1609_04493_b200.model_io)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--gather", action="store_true", help="time a final all-gather of tau (off the hot path)")
@@ -237,7 +259,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = dict(synth.CONFIGS[args.config], name=args.config)
+    cfg = config_of(args)
     n = cfg["n"]
     fd = args.config == "C4"
     from paper_1609_04493_b200.sharding import shard_range, gather_rows
@@ -245,7 +267,7 @@ def main():
     total = per_gpu * world if args.scaling == "weak" else per_gpu
     b0, b1 = shard_range(total, world, rank)       # contiguous global-index shard
     per_gpu = b1 - b0
-    robot = synth.robot_for(cfg)
+    robot = robot_of(cfg)
     g = cfg["gravity"]
     dt = torch.float64 if args.dtype == "f64" else torch.float32
     # inputs: a pure function of the GLOBAL state index (any shard regenerates its slice)
@@ -350,9 +372,9 @@ def main():
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak" if args.scaling == "weak" else "strong", "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic",
-        "config": {"workload": f"{args.config}: {'FD (ABA)' if fd else 'RNEA'} n={n} random serial chain, "
-                               f"{per_gpu} states per GPU" if cfg['robot'] == 'random' else
-                               f"{args.config}: {cfg['robot']} n={n}, {per_gpu} states per GPU",
+        "config": {"workload": f"{cfg['name']}: {'FD (ABA)' if fd else 'RNEA'} n={n} random serial chain, "
+                               f"{per_gpu} states per GPU" if cfg['robot'] == 'random' and 'model' not in cfg else
+                               f"{cfg['name']}: {cfg['robot']} n={n}, {per_gpu} states per GPU",
                    "n": n, "states_per_gpu": per_gpu, "global_batch": total, "gather_ms": gather_ms,
                    "parallelism": f"batch-sharded x{world} (no collective on the hot path)",
                    "strategy": strat, "robot_seed": 1000 + n if cfg["robot"] == "random" else cfg["robot"],
