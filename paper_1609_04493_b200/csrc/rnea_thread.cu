@@ -146,10 +146,24 @@ template <> struct TmemIO<float> {
 #ifndef RD_STASH_VEC
 #define RD_STASH_VEC 1
 #endif
-template <typename T, int W> struct StepCfg { static constexpr int kPD = 2, kUnroll = 1; };
-template <> struct StepCfg<double, 8> { static constexpr int kPD = RD_PD64, kUnroll = RD_U64; };
-template <> struct StepCfg<float, 8> { static constexpr int kPD = RD_PD32, kUnroll = RD_U32; };
-template <> struct StepCfg<float, 16> { static constexpr int kPD = RD_PD32, kUnroll = RD_U32; };
+// kFwdFirst: issue the forward link before the backward one in a step (fp32 -3 %,
+// fp64 +5 %, measured).
+template <typename T, int W> struct StepCfg {
+  static constexpr int kPD = 2, kUnroll = 1;
+  static constexpr bool kFwdFirst = false;
+};
+template <> struct StepCfg<double, 8> {
+  static constexpr int kPD = RD_PD64, kUnroll = RD_U64;
+  static constexpr bool kFwdFirst = false;
+};
+template <> struct StepCfg<float, 8> {
+  static constexpr int kPD = RD_PD32, kUnroll = RD_U32;
+  static constexpr bool kFwdFirst = true;
+};
+template <> struct StepCfg<float, 16> {
+  static constexpr int kPD = RD_PD32, kUnroll = RD_U32;
+  static constexpr bool kFwdFirst = true;
+};
 
 template <typename T, int PD>
 struct FwdState {
@@ -440,8 +454,13 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
         const int slot = bpar ? k : n - 1 - k;
         T cur[8], st[8];
         get_smem(slot, cur);
-        bwd_link<PR>(g, P, B, n - 1 - k, cur, tau);
-        fwd_link<PR>(f, P, B, k, st);
+        if constexpr (Cfg::kFwdFirst) {                 // order of the two chains in the step
+          fwd_link<PR>(f, P, B, k, st);
+          bwd_link<PR>(g, P, B, n - 1 - k, cur, tau);
+        } else {
+          bwd_link<PR>(g, P, B, n - 1 - k, cur, tau);
+          fwd_link<PR>(f, P, B, k, st);
+        }
         put_smem(slot, st);
       };
       auto tmem_seg = [&](int k0, int k1) {
@@ -457,8 +476,13 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
           T cur[8], st[8];
           TmemIO<T>::unpack(r, cur);
           TmemIO<T>::ld(tbase + (uint32_t)(slot_nx * KC), r);       // next step's slot, in flight
-          bwd_link<PR>(g, P, B, n - 1 - k, cur, tau);
-          fwd_link<PR>(f, P, B, k, st);
+          if constexpr (Cfg::kFwdFirst) {                 // order of the two chains in the step
+            fwd_link<PR>(f, P, B, k, st);
+            bwd_link<PR>(g, P, B, n - 1 - k, cur, tau);
+          } else {
+            bwd_link<PR>(g, P, B, n - 1 - k, cur, tau);
+            fwd_link<PR>(f, P, B, k, st);
+          }
           TmemIO<T>::st(tbase + (uint32_t)(slot * KC), st);
         }
         TmemIO<T>::wait(r);
