@@ -339,14 +339,16 @@ def main():
 
     # e2e: through the public host-buffer API (pinned host arrays, H2D + kernel + D2H per step)
     e2e = None
-    if not fd and args.dtype == "f64" and args.e2e_steps > 0:
-        pq, pqd, pqdd = (torch.from_numpy(x).pin_memory() for x in (q, qd, qdd))
+    if args.dtype == "f64" and args.e2e_steps > 0:
+        third = tau_in.cpu().numpy() if fd else qdd                # FD: the consistent torques
+        pq, pqd, pqdd = (torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (q, qd, third))
         pout = torch.empty_like(pq).pin_memory()
-        rd.inverse_dynamics_host(model, pq, pqd, pqdd, pout)
+        host_api = rd.forward_dynamics_host if fd else rd.inverse_dynamics_host
+        host_api(model, pq, pqd, pqdd, pout)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            rd.inverse_dynamics_host(model, pq, pqd, pqdd, pout)
+            host_api(model, pq, pqd, pqdd, pout)
         e2e_s = time.perf_counter() - t0
         if world > 1:
             import torch.distributed as dist
@@ -355,7 +357,8 @@ def main():
             e2e_s = float(tt[0])
         e2e = {"value": total * args.e2e_steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": 3 * n * total * 8, "d2h_bytes_per_step": n * total * 8,
-               "api": "rd_inverse_dynamics_host_f64 (pinned host buffers, chunked 2-stream pipeline)"}
+               "api": ("rd_forward_dynamics_host_f64" if fd else "rd_inverse_dynamics_host_f64")
+                      + " (pinned host buffers, chunked 2-stream pipeline)"}
 
     if rank != 0:
         if world > 1:

@@ -182,6 +182,10 @@ rd_status_t rd_forward_dynamics_ex_f32(rd_model_t m, int64_t batch, const float*
  * and returns after tau is complete in host memory (synchronous). */
 rd_status_t rd_inverse_dynamics_host_f64(rd_model_t m, int64_t batch, const double* q,
                                          const double* qd, const double* qdd, double* tau);
+/* Forward dynamics on HOST float64 arrays [n][batch] (same pipeline and rules as
+ * rd_inverse_dynamics_host_f64; the model's FD algorithm). */
+rd_status_t rd_forward_dynamics_host_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                         const double* tau, double* qdd);
 
 /* Number of kernel launches the last rd_* compute call on this thread enqueued. */
 int32_t rd_last_launch_count(void);

@@ -19,7 +19,7 @@ import os
 
 import numpy as np
 
-__all__ = ["Model", "inverse_dynamics", "forward_dynamics", "inverse_dynamics_host", "lib",
+__all__ = ["Model", "inverse_dynamics", "forward_dynamics", "inverse_dynamics_host", "forward_dynamics_host", "lib",
            "RdError", "STRATEGIES", "last_launch_count", "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librd.so")
@@ -37,7 +37,7 @@ EXPORTS = [
     "rd_forward_dynamics_f32", "rd_model_set_fd_algo", "rd_inverse_dynamics_host_f64",
     "rd_last_launch_count", "rd_forward_dynamics_ex_f64", "rd_forward_dynamics_ex_f32",
     "rd_inverse_dynamics_bnd_f64", "rd_inverse_dynamics_bnd_f32", "rd_forward_dynamics_bnd_f64",
-    "rd_forward_dynamics_bnd_f32",
+    "rd_forward_dynamics_bnd_f32", "rd_forward_dynamics_host_f64",
 ]
 
 
@@ -78,6 +78,7 @@ def lib():
         for name in ("rd_forward_dynamics_bnd_f64", "rd_forward_dynamics_bnd_f32"):
             getattr(L, name).argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.rd_inverse_dynamics_host_f64.argtypes = [vp, i64, vp, vp, vp, vp]
+        L.rd_forward_dynamics_host_f64.argtypes = [vp, i64, vp, vp, vp, vp]
         L.rd_last_launch_count.restype = i32
         for name in EXPORTS:
             if name not in ("rd_version", "rd_last_error", "rd_model_n", "rd_model_resolve_strategy",
@@ -248,23 +249,33 @@ def forward_dynamics(model: Model, q, qd, tau, out=None, stream=None, status=Non
     return out
 
 
+def _host_ptr(x):
+    if isinstance(x, np.ndarray):
+        if x.dtype != np.float64 or not x.flags.c_contiguous:
+            raise RdError("host arrays must be C-contiguous float64")
+        return x.ctypes.data
+    if x.dtype.__str__() != "torch.float64" or x.is_cuda or not x.is_contiguous():
+        raise RdError("host tensors must be contiguous CPU float64")
+    return x.data_ptr()
+
+
+def _host_call(fn, name, model, a, b, c, out):
+    B = a.shape[1]
+    if out is None:
+        out = np.empty_like(np.asarray(a)) if isinstance(a, np.ndarray) else a.new_empty(a.shape)
+    _check(fn(model.handle, B, _host_ptr(a), _host_ptr(b), _host_ptr(c), _host_ptr(out)), name)
+    return out
+
+
 def inverse_dynamics_host(model: Model, q, qd, qdd, out=None):
     """End-to-end ID on HOST float64 arrays [n, B] (numpy or CPU torch, pinned preferred).
 
     The library pipelines H2D copies, kernels and D2H copies on its own streams
     and returns when tau is in host memory (rd_inverse_dynamics_host_f64).
     """
-    def ptr(x):
-        if isinstance(x, np.ndarray):
-            if x.dtype != np.float64 or not x.flags.c_contiguous:
-                raise RdError("host arrays must be C-contiguous float64")
-            return x.ctypes.data
-        if x.dtype.__str__() != "torch.float64" or x.is_cuda or not x.is_contiguous():
-            raise RdError("host tensors must be contiguous CPU float64")
-        return x.data_ptr()
-    B = q.shape[1]
-    if out is None:
-        out = np.empty_like(np.asarray(q)) if isinstance(q, np.ndarray) else q.new_empty(q.shape)
-    _check(lib().rd_inverse_dynamics_host_f64(model.handle, B, ptr(q), ptr(qd), ptr(qdd), ptr(out)),
-           "rd_inverse_dynamics_host_f64")
-    return out
+    return _host_call(lib().rd_inverse_dynamics_host_f64, "rd_inverse_dynamics_host_f64", model, q, qd, qdd, out)
+
+
+def forward_dynamics_host(model: Model, q, qd, tau, out=None):
+    """End-to-end FD on HOST float64 arrays [n, B] (rd_forward_dynamics_host_f64)."""
+    return _host_call(lib().rd_forward_dynamics_host_f64, "rd_forward_dynamics_host_f64", model, q, qd, tau, out)

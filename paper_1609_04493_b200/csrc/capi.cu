@@ -170,6 +170,7 @@ struct rd_model_s {
   size_t hbuf_bytes = 0;
   int64_t hchunk = 0;
   cudaStream_t hstream[2] = {nullptr, nullptr};
+  cudaEvent_t hevent[2] = {nullptr, nullptr};   // kernel-order chain across the two host streams
   std::mutex mu;
 };
 
@@ -808,6 +809,7 @@ rd_status_t rd_model_destroy(rd_model_t m) {
   for (int k = 0; k < 2; ++k) {
     if (m->hbuf[k]) cudaFree(m->hbuf[k]);
     if (m->hstream[k]) cudaStreamDestroy(m->hstream[k]);
+    if (m->hevent[k]) cudaEventDestroy(m->hevent[k]);
   }
   delete m;
   return RD_OK;
@@ -899,8 +901,14 @@ rd_status_t rd_forward_dynamics_ex_f32(rd_model_t m, int64_t batch, const float*
 // Host-buffer pipeline: chunks of `hchunk` states; chunk k uses device buffer
 // set k%2 and stream k%2: H2D(q,qd,qdd) -> kernel -> D2H(tau).  Two streams
 // overlap chunk k+1's copies with chunk k's kernel (PCIe is full duplex).
-rd_status_t rd_inverse_dynamics_host_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
-                                         const double* qdd, double* tau) {
+}  // extern "C"
+
+namespace {
+// FD: false = inverse dynamics (third input qdd, output tau), true = forward
+// dynamics (third input tau, output qdd; the model's FD algorithm).
+template <bool FD>
+rd_status_t host_pipeline(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                          const double* qdd, double* tau) {
   g_launches = 0;
   rd_status_t st = check_io<double>(m, batch, q, qd, qdd, tau, false);
   if (st != RD_OK || batch == 0) return st;
@@ -913,7 +921,8 @@ rd_status_t rd_inverse_dynamics_host_f64(rd_model_t m, int64_t batch, const doub
   // evals/s at C3, PCIe-bound at ~50 GB/s H2D): small enough that the pipeline fill/drain
   // (first H2D, last kernel + D2H) is a few % of a 10^6-state call, large enough to amortise
   // the per-copy overhead (RD_HOST_CHUNK_MB overrides, for measurement)
-  static const int64_t chunk_mb = getenv("RD_HOST_CHUNK_MB") ? atoll(getenv("RD_HOST_CHUNK_MB")) : 32;
+  const char* env_chunk = getenv("RD_HOST_CHUNK_MB");
+  const int64_t chunk_mb = env_chunk ? std::max<int64_t>(1, atoll(env_chunk)) : 32;
   const int64_t chunk = std::min<int64_t>(batch, std::max<int64_t>(4096, (chunk_mb << 20) / (8ll * n)));
   const size_t set_bytes = (size_t)4 * n * chunk * sizeof(double);
   if (m->hbuf_bytes < set_bytes) {
@@ -928,11 +937,16 @@ rd_status_t rd_inverse_dynamics_host_f64(rd_model_t m, int64_t batch, const doub
     }
     m->hbuf_bytes = set_bytes;
   }
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < 2; ++k) {
     if (!m->hstream[k]) {
       cudaError_t e = cudaStreamCreateWithFlags(&m->hstream[k], cudaStreamNonBlocking);
       if (e != cudaSuccess) return cuda_fail(e, "stream create");
     }
+    if (!m->hevent[k]) {
+      cudaError_t e = cudaEventCreateWithFlags(&m->hevent[k], cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e, "event create");
+    }
+  }
   int launches = 0;
   for (int64_t b0 = 0, k = 0; b0 < batch; b0 += chunk, ++k) {
     const int64_t bc = std::min(chunk, batch - b0);
@@ -947,11 +961,19 @@ rd_status_t rd_inverse_dynamics_host_f64(rd_model_t m, int64_t batch, const doub
     if (e == cudaSuccess) e = cudaMemcpy2DAsync(dqd, dp, qd + b0, hp, dp, n, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemcpy2DAsync(dqdd, dp, qdd + b0, hp, dp, n, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return cuda_fail(e, "host path H2D");
+    // kernels run in chunk order: the kernels that use the model workspace
+    // (GENERIC ID, the FD algorithms) must not overlap across the two streams;
+    // the copies still overlap the neighbouring chunks' kernels
+    if (k > 0) e = cudaStreamWaitEvent(s, m->hevent[(k - 1) & 1], 0);
+    if (e != cudaSuccess) return cuda_fail(e, "host path event wait");
     m->mu.unlock();
-    st = inverse_dynamics<double>(m, bc, dq, dqd, dqdd, dtau, s);
+    st = FD ? forward_dynamics<double>(m, bc, dq, dqd, dqdd, dtau, s)
+            : inverse_dynamics<double>(m, bc, dq, dqd, dqdd, dtau, s);
     m->mu.lock();
     launches += g_launches;
     if (st != RD_OK) return st;
+    e = cudaEventRecord(m->hevent[k & 1], s);
+    if (e != cudaSuccess) return cuda_fail(e, "host path event record");
     e = cudaMemcpy2DAsync(tau + b0, hp, dtau, dp, dp, n, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_fail(e, "host path D2H");
   }
@@ -961,6 +983,17 @@ rd_status_t rd_inverse_dynamics_host_f64(rd_model_t m, int64_t batch, const doub
   }
   g_launches = launches;
   return RD_OK;
+}
+}  // namespace
+
+extern "C" {
+rd_status_t rd_inverse_dynamics_host_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                         const double* qdd, double* tau) {
+  return host_pipeline<false>(m, batch, q, qd, qdd, tau);
+}
+rd_status_t rd_forward_dynamics_host_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
+                                         const double* tau, double* qdd) {
+  return host_pipeline<true>(m, batch, q, qd, tau, qdd);
 }
 
 }  // extern "C"

@@ -325,6 +325,25 @@ def test_host_path_equals_device_path(rd):
     np.testing.assert_array_equal(out.numpy(), dev_tau)
 
 
+def test_host_path_multichunk_workspace_kernels(rd, monkeypatch):
+    # small chunks: many chunks alternate between the two host streams; GENERIC ID
+    # (screw joint) and the FD algorithms share the model workspace across chunks
+    monkeypatch.setenv("RD_HOST_CHUNK_MB", "1")
+    r = synth.random_chain(10, 1313, prismatic_fraction=0.3)
+    i = int(np.argmax(np.linalg.norm(r["S"][:, 3:], axis=1)))
+    r["S"][i, :3] += 0.2 * r["S"][i, 3:]                    # screw joint -> GENERIC / joint-frame ABA
+    q, qd, qdd = synth.states(18, 10, 0, 60000)
+    model = rd.Model.from_robot(r, synth.GRAVITY_Z)
+    dev_tau = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd)).cpu().numpy()
+    np.testing.assert_array_equal(rd.inverse_dynamics_host(model, q, qd, qdd), dev_tau)
+    for algo in ("aba", "jsiia", "aba_scan"):
+        model.set_fd_algo(algo)
+        dev_qdd = rd.forward_dynamics(model, dev(q), dev(qd), dev(dev_tau)).cpu().numpy()
+        host_qdd = rd.forward_dynamics_host(model, q, qd, dev_tau)
+        np.testing.assert_array_equal(host_qdd, dev_qdd)
+        assert rel_err_per_state(host_qdd, qdd, floor=1.0).max() < 1e-8
+
+
 def test_launch_count_and_errors(rd):
     model = rd.Model.from_robot(synth.random_chain(30, 1030), synth.GRAVITY_Z)
     q = torch.zeros((30, 1000), dtype=torch.float64, device="cuda")
