@@ -20,7 +20,7 @@ LIB = os.path.join(HERE, "librd.so")
 BUILD = os.path.join(ROOT, "build", "rd")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v",
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-Wall,-Wshadow", "-Xptxas", "-v",
                      f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 
 

@@ -9,7 +9,7 @@ mkdir -p fakebuild/obj
 objs=()
 for o in build/rd/*.o; do
   if [ "$(basename $o)" = "$src.o" ]; then
-    nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 \
+    nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2,-Wall,-Wshadow \
       -Iinclude -Ipaper_1609_04493_b200/csrc "$@" -c paper_1609_04493_b200/csrc/$src -o fakebuild/obj/$src.o
     objs+=(fakebuild/obj/$src.o)
   else
