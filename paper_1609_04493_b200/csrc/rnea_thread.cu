@@ -127,7 +127,7 @@ template <> struct TmemIO<float> {
 // MOVs and the back-edge carried ~20 % long-scoreboard stalls).  Measured on
 // B200: fp64 n = 30 (W = 8), 1M states 0.543 -> 0.494 ms with
 // (8, 4); fp32 n = 30 (W = 16) 0.312 -> 0.309 ms with (4, 2); the 16-warp fp64
-// plan (n <= 15, 128-register cap) keeps (2, 1).
+// plan (n <= 15, 128-register cap) also (4, 2): n = 15, 1M 0.227 -> 0.222 ms.
 #ifndef RD_PD64
 #define RD_PD64 8
 #endif
@@ -148,8 +148,14 @@ template <> struct TmemIO<float> {
 #endif
 // kFwdFirst: issue the forward link before the backward one in a step (fp32 -3 %,
 // fp64 +5 %, measured).
+#ifndef RD_PD64W16
+#define RD_PD64W16 4
+#endif
+#ifndef RD_U64W16
+#define RD_U64W16 2
+#endif
 template <typename T, int W> struct StepCfg {
-  static constexpr int kPD = 2, kUnroll = 1;
+  static constexpr int kPD = RD_PD64W16, kUnroll = RD_U64W16;
   static constexpr bool kFwdFirst = false;
 };
 template <> struct StepCfg<double, 8> {

@@ -14,13 +14,19 @@ ap.add_argument("--fd", action="store_true")
 ap.add_argument("--strategy", default="thread")
 ap.add_argument("--fd-algo", default="aba")
 ap.add_argument("--dtype", default="f64")
+ap.add_argument("--n", type=int, default=0, help="random chain with n links (overrides the config)")
+ap.add_argument("--batch", type=int, default=0)
 a = ap.parse_args()
 rd.LIB_PATH = a.lib
 import torch  # noqa: E402
 import synth  # noqa: E402
 from quick_time import time_call  # noqa: E402
 
-cfg = synth.CONFIGS[a.config]
+cfg = dict(synth.CONFIGS[a.config])
+if a.n:
+    cfg.update(n=a.n, robot="random")
+if a.batch:
+    cfg.update(batch=a.batch)
 n = cfg["n"]
 dt = torch.float64 if a.dtype == "f64" else torch.float32
 q, qd, qdd = synth.states(cfg["seed"], n, 0, cfg["batch"], cfg["ranges"])
@@ -30,4 +36,5 @@ m.set_strategy(a.strategy)
 m.set_fd_algo(a.fd_algo)
 out = torch.empty_like(tq)
 f = (lambda: rd.forward_dynamics(m, tq, tqd, tqdd, out)) if a.fd else (lambda: rd.inverse_dynamics(m, tq, tqd, tqdd, out))
-print(os.path.basename(a.lib), a.config, "fd" if a.fd else "id", f"{time_call(f, reps=50):.4f} ms")
+print(os.path.basename(a.lib), a.config, f"n={n} B={cfg['batch']}", "fd" if a.fd else "id",
+      f"{time_call(f, reps=50):.4f} ms")
