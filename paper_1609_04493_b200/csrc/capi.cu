@@ -404,7 +404,7 @@ template <> const rd::Boundary<float>& bnd<float>(rd_model_t m) { return m->b32;
 //    link, log-depth shuffle scans; the latency regime (paper P:505/P:524), e.g.
 //    n = 30, B = 2048: 26 us vs 29 us (REVERSE) and 39 us (THREAD);
 //  * batch above the thread crossover (fp64 32768, fp32 49152) and the on-chip
-//    stash fits (n <= 30 fp64 / 32 fp32) -> THREAD: e.g. n = 30, B = 1M: 3.9x
+//    stash fits (n <= 30 fp64 / 32 fp32) -> THREAD: e.g. n = 30, B = 1M: 6.3x
 //    WARP_SCAN; below it one tile per SM is latency-bound (2n serial link steps),
 //    and the 16-warp stash-free REVERSE wins (n = 30, B = 16384: 30 vs 39 us);
 //  * n > 32 and batch <= 1024 -> BLOCK_SCAN: one CTA per state (NEXT-3), e.g.
