@@ -29,10 +29,13 @@ constexpr int kRevThreads = 128;
 #ifndef RD_REV_U
 #define RD_REV_U 4
 #endif
+#ifndef RD_REV_MB
+#define RD_REV_MB 4
+#endif
 constexpr int kRevPD = RD_REV_PD, kRevU = RD_REV_U;
 
 template <typename T, bool PR, bool SB>
-__global__ void __launch_bounds__(kRevThreads, 4)
+__global__ void __launch_bounds__(kRevThreads, RD_REV_MB)
 rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
                 const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
                 T* __restrict__ tau, const unsigned char* __restrict__ prism_g,
@@ -157,7 +160,7 @@ static cudaError_t launch_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& 
     if (e != cudaSuccess) return e;
   }
   int64_t grid = (B + kRevThreads - 1) / kRevThreads;
-  const int64_t cap = (int64_t)num_sms() * 4;
+  const int64_t cap = (int64_t)num_sms() * RD_REV_MB;
   if (grid > cap) grid = cap;
   rnea_rev_kernel<T, PR, SB><<<(unsigned)grid, kRevThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau, prism,
                                                                          sb);
