@@ -156,24 +156,35 @@ class Model:
             pass
 
 
-def _stream_ptr(stream):
+def _stream_ptr(stream, device_index=None):
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return ctypes.c_void_p(s.cuda_stream)
+    if stream is not None:
+        return stream.cuda_stream
+    # the current stream's raw handle without constructing a torch.cuda.Stream
+    # object (the binding's own cost dominated small-batch calls, tools/host_overhead.py)
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None and device_index is not None:
+        return raw(device_index)
+    return torch.cuda.current_stream().cuda_stream
 
 
 def _check_tensors(model: Model, *ts):
+    """Marshalling checks only: CUDA, fp64/fp32, one device, contiguous [n, B]."""
     import torch
     t0 = ts[0]
+    dt = t0.dtype
     if not t0.is_cuda:
         raise RdError("inputs must be CUDA tensors (use inverse_dynamics_host for host arrays)")
-    if t0.dtype not in (torch.float64, torch.float32):
+    if dt is not torch.float64 and dt is not torch.float32:
         raise RdError("dtype must be float64 or float32")
+    dev = t0.get_device()
+    shape = t0.shape
+    if len(shape) != 2 or shape[0] != model.n:
+        raise RdError("tensors must be contiguous [n, B] with one dtype/device")
     for t in ts:
-        if t.dtype != t0.dtype or t.device != t0.device or t.dim() != 2 or t.shape[0] != model.n \
-                or t.shape[1] != t0.shape[1] or not t.is_contiguous():
+        if t.dtype is not dt or t.get_device() != dev or t.shape != shape or not t.is_contiguous():
             raise RdError("tensors must be contiguous [n, B] with one dtype/device")
-    return t0.dtype
+    return dt
 
 
 def _boundary_ptrs(boundary, ref):
@@ -208,9 +219,12 @@ def inverse_dynamics(model: Model, q, qd, qdd, out=None, stream=None, boundary=N
         _check(f(model.handle, q.shape[1], q.data_ptr(), qd.data_ptr(), qdd.data_ptr(), v0, vd0, ft,
                  out.data_ptr(), _stream_ptr(stream)), "rd_inverse_dynamics_bnd")
         return out
-    f = lib().rd_inverse_dynamics_f64 if dt == torch.float64 else lib().rd_inverse_dynamics_f32
-    _check(f(model.handle, q.shape[1], q.data_ptr(), qd.data_ptr(), qdd.data_ptr(), out.data_ptr(),
-             _stream_ptr(stream)), "rd_inverse_dynamics")
+    L = lib()
+    f = L.rd_inverse_dynamics_f64 if dt is torch.float64 else L.rd_inverse_dynamics_f32
+    rc = f(model.handle, q.shape[1], q.data_ptr(), qd.data_ptr(), qdd.data_ptr(), out.data_ptr(),
+           _stream_ptr(stream, q.get_device()))
+    if rc:
+        _check(rc, "rd_inverse_dynamics")
     return out
 
 
@@ -238,7 +252,7 @@ def forward_dynamics(model: Model, q, qd, tau, out=None, stream=None, status=Non
     if status is None:
         f = lib().rd_forward_dynamics_f64 if dt == torch.float64 else lib().rd_forward_dynamics_f32
         _check(f(model.handle, q.shape[1], q.data_ptr(), qd.data_ptr(), tau.data_ptr(), out.data_ptr(),
-                 _stream_ptr(stream)), "rd_forward_dynamics")
+                 _stream_ptr(stream, q.get_device())), "rd_forward_dynamics")
         return out
     if status.dtype != torch.int32 or status.device != q.device or status.shape != (q.shape[1],) \
             or not status.is_contiguous():
