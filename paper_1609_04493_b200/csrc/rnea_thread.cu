@@ -9,13 +9,17 @@
 //    scalars, lives ON CHIP: the first `lt` links in Tensor Memory (tcgen05.st /
 //    tcgen05.ld, 32x32b shape: warp w owns TMEM lanes 32(w%4).., and columns
 //    [(w/4) * 2048/W, ...)), the remaining n - lt links in shared memory laid
-//    out [link][8][thread] (conflict-free, 256 B per warp access);
+//    out [link][8/VW][thread] of 16-byte vectors (conflict-free);
+//  * ping-pong: the backward sweep of tile t-1 and the forward sweep of tile t
+//    share each loop step and the stash slots (below);
 //  * model constants are a __grid_constant__ kernel parameter indexed by the
 //    (warp-uniform) link counter: uniform constant-bank loads;
-//  * inputs q, qd, qdd are read coalesced (x[i*B + b]) two links ahead of use;
-//    tau is written coalesced during the backward sweep;
-//  * the loops are rolled (unroll 2): the whole kernel stays in the instruction
-//    cache (a fully unrolled n = 30 body thrashed it, profiles/r01).
+//  * inputs q, qd, qdd are read coalesced (x[i*B + b]) kPD links ahead of use
+//    (streaming across the tile boundary), the step loops unrolled by a divisor
+//    of kPD (StepCfg); tau is written coalesced one backward step late;
+//  * the link loops stay rolled (besides that unroll): the whole kernel stays in
+//    the instruction cache (a fully unrolled n = 30 body thrashed it, profiles/r01);
+//  * instantiations: precision x W x prismatic joints (PR) x per-state boundary (SB).
 #include <cuda_runtime.h>
 #include <type_traits>
 #include <cstdint>
