@@ -254,9 +254,9 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
         T Vn[6];
         if constexpr (PR) {
           const bool pz = PRs[i];
-          T s, c, lp1, lp2;
-          dh_link<PR>(C, pz, cq, &s, &c, &lp1, &lp2);
-          dh_ad_finv(C.ca, C.sa, C.p0, lp1, lp2, s, c, V, Vn);
+          T s, c, dl;
+          dh_link<PR>(C, pz, cq, &s, &c, &dl);
+          dh_ad_finv(C.ca, C.sa, C.a, dl, s, c, V, Vn);
           Vn[5] += pz ? T(0) : cqd;
           Vn[2] += pz ? cqd : T(0);
         } else {
@@ -287,18 +287,18 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
       const T nq = __ldg(pq + o), nqd = __ldg(pqd + o), nt = __ldg(pt + o);
       const LinkDH<T>& C = L[i];
       const bool pz = PR && PRs[i];
-      T s, c, lp1, lp2;
+      T s, c, dl;
       const T qdi = cqd;
       T cc[6];
       if constexpr (PR) {
-        dh_link<PR>(C, pz, cq, &s, &c, &lp1, &lp2);
+        dh_link<PR>(C, pz, cq, &s, &c, &dl);
         // c_i = ad_V(S qd), S qd = (sp e_z, sr e_z)
         const T sr = pz ? T(0) : qdi, sp = pz ? qdi : T(0);
         cc[0] = fma(sp, V[4], sr * V[1]); cc[1] = -fma(sp, V[3], sr * V[0]); cc[2] = 0;
         cc[3] = sr * V[4]; cc[4] = -sr * V[3]; cc[5] = 0;
       } else {
         dh_sincos(C, cq, &s, &c);
-        lp1 = C.p1; lp2 = C.p2;
+        dl = C.d;
         cc[0] = qdi * V[1]; cc[1] = -qdi * V[0]; cc[2] = 0; cc[3] = qdi * V[4]; cc[4] = -qdi * V[3]; cc[5] = 0;
       }
       T ph[6];
@@ -330,11 +330,11 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
         for (int k = 0; k < 6; ++k) pa[k] = ph[k] + Kcc[k] + U[k] * ub;
         Kc = K;
         if constexpr (PR) {
-          dh_congruence(C.ca, C.sa, C.p0, lp1, lp2, s, c, Kc);
-          dh_bwd(C.ca, C.sa, C.p0, lp1, lp2, s, c, pa, zero6, pc);
+          dh_congruence(C.ca, C.sa, C.a, dl, s, c, Kc);
+          dh_bwd(C.ca, C.sa, C.a, dl, s, c, pa, zero6, pc);
         } else {
           dh_congruence(C, s, c, Kc);
-          dh_bwd(C.ca, C.sa, C.p0, C.p1, C.p2, s, c, pa, zero6, pc);
+          dh_bwd(C.ca, C.sa, C.a, C.d, s, c, pa, zero6, pc);
         }
         T x[6];
 #pragma unroll
@@ -342,7 +342,7 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
         if constexpr (PR) {
           x[5] -= pz ? T(0) : qdi;
           x[2] -= pz ? qdi : T(0);
-          dh_ad_f(C.ca, C.sa, C.p0, lp1, lp2, s, c, x, V);   // V_{i-1} = Ad_{f_i}(V_i - S qd)
+          dh_ad_f(C.ca, C.sa, C.a, dl, s, c, x, V);   // V_{i-1} = Ad_{f_i}(V_i - S qd)
         } else {
           x[5] -= qdi;
           dh_ad_f(C, s, c, x, V);
@@ -411,13 +411,13 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
         const T qdi = cqd3;
         T Vn[6], an[6];
         if constexpr (PR) {
-          T s, c, lp1, lp2;
-          dh_link<PR>(C, pz, cq3, &s, &c, &lp1, &lp2);
+          T s, c, dl;
+          dh_link<PR>(C, pz, cq3, &s, &c, &dl);
           const T sr = pz ? T(0) : qdi, sp = pz ? qdi : T(0);
-          dh_ad_finv(C.ca, C.sa, C.p0, lp1, lp2, s, c, V, Vn);
+          dh_ad_finv(C.ca, C.sa, C.a, dl, s, c, V, Vn);
           Vn[5] += sr;
           Vn[2] += sp;
-          dh_ad_finv(C.ca, C.sa, C.p0, lp1, lp2, s, c, a, an);
+          dh_ad_finv(C.ca, C.sa, C.a, dl, s, c, a, an);
           an[0] = fma(sr, Vn[1], fma(sp, Vn[4], an[0]));
           an[1] = fma(-sr, Vn[0], fma(-sp, Vn[3], an[1]));
           an[3] = fma(sr, Vn[4], an[3]);

@@ -299,7 +299,7 @@ bool build_dh(rd_model_t m, const std::vector<Rigid>& Mp, const std::vector<std:
       }
     rd::LinkDH<double>& L = m->D64[i];
     L.ca = ca; L.sa = sa;
-    L.p0 = a; L.p1 = -sa * d; L.p2 = ca * d;
+    L.a = a; L.d = d;
     L.th0 = std::atan2(st, ct);
     L.cth0 = std::cos(L.th0);
     L.sth0 = std::sin(L.th0);
@@ -312,7 +312,7 @@ bool build_dh(rd_model_t m, const std::vector<Rigid>& Mp, const std::vector<std:
     L.I[4] = 0.5 * (Jd[3][5] + Jd[5][3]);
     L.I[5] = 0.5 * (Jd[4][5] + Jd[5][4]);
     rd::LinkDH<float>& F = m->D32[i];
-    F.ca = (float)L.ca; F.sa = (float)L.sa; F.p0 = (float)L.p0; F.p1 = (float)L.p1; F.p2 = (float)L.p2;
+    F.ca = (float)L.ca; F.sa = (float)L.sa; F.a = (float)L.a; F.d = (float)L.d;
     F.th0 = (float)L.th0; F.m = (float)L.m;
     F.cth0 = (float)L.cth0; F.sth0 = (float)L.sth0;
     for (int k = 0; k < 3; ++k) F.h[k] = (float)L.h[k];

@@ -140,9 +140,8 @@ __device__ __forceinline__ void link_transform(const LinkConst<T>& C, T qi, Rot<
 namespace rd {
 
 // ---------------------------------------------------------------- DH-frame congruence
-// X^T K X for X = Ad_{f^-1}, f = (Rx(alpha) Rz(theta), p): rotate the blocks by
-// Rz(theta), then by Rx(alpha) (each a plane rotation: ~14 flops per symmetric
-// block, 24 per general block), then the p-shift of congruence() above.
+// Plane rotations of the 3x3 blocks (~14 flops per symmetric block, 24 per
+// general block), the rotation factors of dh_congruence below.
 template <typename T>
 __device__ __forceinline__ void sym_rot_plane(T* a, int i, int j, int k, T c, T s) {
   // symmetric block in (xx yy zz xy xz yz) storage; rotate the (i, j) plane, k the fixed axis
@@ -171,50 +170,64 @@ __device__ __forceinline__ void gen_rot_plane(T* b, int i, int j, T c, T s) {
     b[3 * r + j] = fma(s, bi, c * bj);
   }
 }
+// Congruence by a translation t along one axis, C_t(K) = Ad_{(I,t)^-1}^T K Ad_{(I,t)^-1}:
+//   B <- B - A[t],  C <- C + [t]B + ([t]B)^T - [t]A[t]     (B, the old B on the right)
+// written out for t = d e_z and t = a e_x, where [t] has two non-zeros (17 FP64
+// instructions each instead of ~80 for a general t).
 template <typename T>
-__device__ __forceinline__ void dh_congruence(T ca, T sa, T p0, T p1, T p2, T s, T c, Sym6<T>& K) {
+__device__ __forceinline__ void sym6_shift_z(Sym6<T>& K, T d) {
+  const T* A = K.a;     // xx yy zz xy xz yz
+  T* Bm = K.b;          // row-major
+  T* C = K.c;
+  const T dd = d * d, d2 = d + d;
+  const T b00 = Bm[0], b01 = Bm[1], b02 = Bm[2], b10 = Bm[3], b11 = Bm[4], b12 = Bm[5];
+  C[0] = fma(-d2, b10, fma(dd, A[1], C[0]));
+  C[1] = fma(d2, b01, fma(dd, A[0], C[1]));
+  C[3] = fma(-d, b11, fma(d, b00, fma(-dd, A[3], C[3])));
+  C[4] = fma(-d, b12, C[4]);
+  C[5] = fma(d, b02, C[5]);
+  // B(:, 0) -= d A(:, 1);  B(:, 1) += d A(:, 0)
+  Bm[0] = fma(-d, A[3], b00); Bm[1] = fma(d, A[0], b01);
+  Bm[3] = fma(-d, A[1], b10); Bm[4] = fma(d, A[3], b11);
+  Bm[6] = fma(-d, A[5], Bm[6]); Bm[7] = fma(d, A[4], Bm[7]);
+}
+template <typename T>
+__device__ __forceinline__ void sym6_shift_x(Sym6<T>& K, T a) {
+  const T* A = K.a;
+  T* Bm = K.b;
+  T* C = K.c;
+  const T aa = a * a, a2 = a + a;
+  const T b10 = Bm[3], b11 = Bm[4], b12 = Bm[5], b20 = Bm[6], b21 = Bm[7], b22 = Bm[8];
+  C[1] = fma(-a2, b21, fma(aa, A[2], C[1]));
+  C[2] = fma(a2, b12, fma(aa, A[1], C[2]));
+  C[5] = fma(-a, b22, fma(a, b11, fma(-aa, A[5], C[5])));
+  C[3] = fma(-a, b20, C[3]);
+  C[4] = fma(a, b10, C[4]);
+  // B(:, 1) -= a A(:, 2);  B(:, 2) += a A(:, 1)
+  Bm[1] = fma(-a, A[4], Bm[1]); Bm[2] = fma(a, A[3], Bm[2]);
+  Bm[4] = fma(-a, A[5], b11);   Bm[5] = fma(a, A[1], b12);
+  Bm[7] = fma(-a, A[2], b21);   Bm[8] = fma(a, A[5], b22);
+}
+
+// X^T K X for X = Ad_{f^-1}, f = Rx(alpha) Tx(a) Rz(theta) Tz(d): the congruences
+// of the four factors, innermost first (C_{gh} = C_g o C_h): shift by d e_z,
+// rotate by Rz(theta), shift by a e_x, rotate by Rx(alpha).
+template <typename T>
+__device__ __forceinline__ void dh_congruence(T ca, T sa, T a, T d, T s, T c, Sym6<T>& K) {
+  sym6_shift_z(K, d);
   // Rz(theta): plane (0, 1), fixed axis 2
   sym_rot_plane(K.a, 0, 1, 2, c, s);
   gen_rot_plane(K.b, 0, 1, c, s);
   sym_rot_plane(K.c, 0, 1, 2, c, s);
+  sym6_shift_x(K, a);
   // Rx(alpha): plane (1, 2), fixed axis 0
   sym_rot_plane(K.a, 1, 2, 0, ca, sa);
   gen_rot_plane(K.b, 1, 2, ca, sa);
   sym_rot_plane(K.c, 1, 2, 0, ca, sa);
-  // p-shift: B_new = B' - A'[p], C_new = C' + [p]B' + ([p]B')^T - [p]A'[p]
-  T Ap[9];
-  sym_full(K.a, Ap);
-  T AP[9];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    AP[3 * i + 0] = Ap[3 * i + 1] * p2 - Ap[3 * i + 2] * p1;
-    AP[3 * i + 1] = Ap[3 * i + 2] * p0 - Ap[3 * i + 0] * p2;
-    AP[3 * i + 2] = Ap[3 * i + 0] * p1 - Ap[3 * i + 1] * p0;
-  }
-  T PB[9], PAP[9];
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    const T x0 = K.b[j], x1 = K.b[3 + j], x2 = K.b[6 + j];
-    PB[j] = p1 * x2 - p2 * x1;
-    PB[3 + j] = p2 * x0 - p0 * x2;
-    PB[6 + j] = p0 * x1 - p1 * x0;
-    const T y0 = AP[j], y1 = AP[3 + j], y2 = AP[6 + j];
-    PAP[j] = p1 * y2 - p2 * y1;
-    PAP[3 + j] = p2 * y0 - p0 * y2;
-    PAP[6 + j] = p0 * y1 - p1 * y0;
-  }
-#pragma unroll
-  for (int k = 0; k < 9; ++k) K.b[k] -= AP[k];
-  K.c[0] += 2 * PB[0] - PAP[0];
-  K.c[1] += 2 * PB[4] - PAP[4];
-  K.c[2] += 2 * PB[8] - PAP[8];
-  K.c[3] += PB[1] + PB[3] - PAP[1];
-  K.c[4] += PB[2] + PB[6] - PAP[2];
-  K.c[5] += PB[5] + PB[7] - PAP[5];
 }
 template <typename T>
 __device__ __forceinline__ void dh_congruence(const LinkDH<T>& C, T s, T c, Sym6<T>& K) {
-  dh_congruence(C.ca, C.sa, C.p0, C.p1, C.p2, s, c, K);
+  dh_congruence(C.ca, C.sa, C.a, C.d, s, c, K);
 }
 
 template <typename T>

@@ -34,7 +34,7 @@ struct LinkConst {
 template <typename T>
 struct LinkDH {
   T ca, sa;       // cos/sin alpha
-  T p0, p1, p2;   // constant translation
+  T a, d;         // DH translations: f = Rx(alpha) Tx(a) Rz(theta) Tz(d), p = (a, -sa d, ca d)
   T th0;          // joint angle offset
   T cth0, sth0;   // cos/sin th0 (fp32 uses the angle-addition form for accuracy at large |q|)
   T m;

@@ -215,68 +215,88 @@ __device__ __forceinline__ void bwd_step(const Rot<T>& R, T p0, T p1, T p2, cons
 }
 
 // ---------------------------------------------------------------- DH frames
-// f = (R, p), R = Rx(alpha) Rz(theta), p = (p0, p1, p2) constant (LinkDH).
-// out = Ad_{f^-1} in = (R^T (v + w x p), R^T w), R^T = Rz^T Rx^T.
+// f = Rx(alpha) Tx(a) Rz(theta) Tz(d) (modified DH), so R = Rx(alpha) Rz(theta)
+// and p = (a, -sa d, ca d).  Every map below is applied as the product of its
+// four elementary factors (plane rotations and single-axis shifts, each 2-8
+// FP64 instructions), never through R and p: Ad_{f^-1} costs 20 instructions
+// per twist (22 with the general p x w form), the backward Ad^T with Fhat folded
+// into its last factor 20 (28).  DESIGN.md "DH frames" derives the factors;
+// the GPU parity suite checks every kernel that uses them against the oracle.
+// out = Ad_{f^-1} in = Ad_{Tz^-1} Ad_{Rz^-1} Ad_{Tx^-1} Ad_{Rx^-1} in.
 template <typename T>
-__device__ __forceinline__ void dh_ad_finv(T ca, T sa, T p0, T p1, T p2, T s, T c, const T* in, T* out) {
-  const T x0 = fma(in[4], p2, fma(-in[5], p1, in[0]));
-  const T x1 = fma(in[5], p0, fma(-in[3], p2, in[1]));
-  const T x2 = fma(in[3], p1, fma(-in[4], p0, in[2]));
-  // Rx^T x = (x0, ca x1 + sa x2, -sa x1 + ca x2); then Rz^T y = (c y0 + s y1, -s y0 + c y1, y2)
-  const T y1 = fma(ca, x1, sa * x2), y2 = fma(ca, x2, -(sa * x1));
-  out[0] = fma(c, x0, s * y1);
-  out[1] = fma(c, y1, -(s * x0));
-  out[2] = y2;
-  const T u1 = fma(ca, in[4], sa * in[5]), u2 = fma(ca, in[5], -(sa * in[4]));
-  out[3] = fma(c, in[3], s * u1);
-  out[4] = fma(c, u1, -(s * in[3]));
-  out[5] = u2;
+__device__ __forceinline__ void dh_ad_finv(T ca, T sa, T a, T d, T s, T c, const T* in, T* out) {
+  // Rx^T (x0, ca x1 + sa x2, -sa x1 + ca x2) on v and w
+  T v1 = fma(ca, in[1], sa * in[2]), v2 = fma(ca, in[2], -(sa * in[1]));
+  const T w1 = fma(ca, in[4], sa * in[5]), w2 = fma(ca, in[5], -(sa * in[4]));
+  // Tx(a)^-1: v += w x (a e_x) = a (0, w2, -w1)
+  v1 = fma(a, w2, v1);
+  v2 = fma(-a, w1, v2);
+  // Rz^T (c y0 + s y1, -s y0 + c y1, y2)
+  const T W0 = fma(c, in[3], s * w1), W1 = fma(c, w1, -(s * in[3]));
+  const T V0 = fma(c, in[0], s * v1), V1 = fma(c, v1, -(s * in[0]));
+  // Tz(d)^-1: v += w x (d e_z) = d (w1, -w0, 0)
+  out[0] = fma(d, W1, V0);
+  out[1] = fma(-d, W0, V1);
+  out[2] = v2;
+  out[3] = W0; out[4] = W1; out[5] = w2;
 }
 template <typename T>
 __device__ __forceinline__ void dh_ad_finv(const LinkDH<T>& C, T s, T c, const T* in, T* out) {
-  dh_ad_finv(C.ca, C.sa, C.p0, C.p1, C.p2, s, c, in, out);
+  dh_ad_finv(C.ca, C.sa, C.a, C.d, s, c, in, out);
 }
 
-// F = Fh + Ad^T_{f^-1} Fn = Fh + (R f, p x (R f) + R m), R = Rx(alpha) Rz(theta)
-// with (ca, sa, p, s, c) of the child link (identity for the tip, A5).
+// F = Fh + Ad^T_{f^-1} Fn, Ad^T_{f^-1} = Ad^T_{Rx^-1} Ad^T_{Tx^-1} Ad^T_{Rz^-1} Ad^T_{Tz^-1}
+// (a translation t acts as (f, m) -> (f, m + t x f)), with (ca, sa, a, d, s, c) of
+// the child link (identity for the tip, A5); Fh is added inside the last factor.
 template <typename T>
-__device__ __forceinline__ void dh_bwd(T ca, T sa, T p0, T p1, T p2, T s, T c, const T* Fn, const T* Fh, T* F) {
-  // Rz y = (c y0 - s y1, s y0 + c y1, y2); Rx z = (z0, ca z1 - sa z2, sa z1 + ca z2)
-  const T a0 = fma(c, Fn[0], -(s * Fn[1])), a1 = fma(s, Fn[0], c * Fn[1]), a2 = Fn[2];
-  const T y0 = a0, y1 = fma(ca, a1, -(sa * a2)), y2 = fma(sa, a1, ca * a2);
-  const T b0 = fma(c, Fn[3], -(s * Fn[4])), b1 = fma(s, Fn[3], c * Fn[4]), b2 = Fn[5];
-  const T z0 = b0, z1 = fma(ca, b1, -(sa * b2)), z2 = fma(sa, b1, ca * b2);
-  F[0] = Fh[0] + y0;
-  F[1] = Fh[1] + y1;
-  F[2] = Fh[2] + y2;
-  F[3] = fma(p1, y2, fma(-p2, y1, Fh[3] + z0));
-  F[4] = fma(p2, y0, fma(-p0, y2, Fh[4] + z1));
-  F[5] = fma(p0, y1, fma(-p1, y0, Fh[5] + z2));
+__device__ __forceinline__ void dh_bwd(T ca, T sa, T a, T d, T s, T c, const T* Fn, const T* Fh, T* F) {
+  // Tz(d): m += d e_z x f = d (-f1, f0, 0)
+  const T m0 = fma(-d, Fn[1], Fn[3]), m1 = fma(d, Fn[0], Fn[4]);
+  // Rz: (c y0 - s y1, s y0 + c y1, y2); the x rows are final (Rx fixes e_x)
+  F[0] = fma(c, Fn[0], fma(-s, Fn[1], Fh[0]));
+  F[3] = fma(c, m0, fma(-s, m1, Fh[3]));
+  const T f1 = fma(s, Fn[0], c * Fn[1]);
+  T n1 = fma(s, m0, c * m1);
+  // Tx(a): m += a e_x x f = a (0, -f2, f1)
+  n1 = fma(-a, Fn[2], n1);
+  const T n2 = fma(a, f1, Fn[5]);
+  // Rx: (z0, ca z1 - sa z2, sa z1 + ca z2), + Fh
+  F[1] = fma(ca, f1, fma(-sa, Fn[2], Fh[1]));
+  F[2] = fma(sa, f1, fma(ca, Fn[2], Fh[2]));
+  F[4] = fma(ca, n1, fma(-sa, n2, Fh[4]));
+  F[5] = fma(sa, n1, fma(ca, n2, Fh[5]));
 }
 
-// out = Ad_f in = (R v + p x (R w), R w), R = Rx(alpha) Rz(theta): the inverse of
-// dh_ad_finv (used to re-derive V_{i-1}, Vdot_{i-1} from V_i, Vdot_i).
+// out = Ad_f in = Ad_{Rx} Ad_{Tx} Ad_{Rz} Ad_{Tz} in (a translation t acts as
+// (v, w) -> (v + t x w, w)): the inverse of dh_ad_finv (used to re-derive
+// V_{i-1}, Vdot_{i-1} from V_i, Vdot_i).
 template <typename T>
-__device__ __forceinline__ void dh_ad_f(T ca, T sa, T p0, T p1, T p2, T s, T c, const T* in, T* out) {
-  // Rz y = (c y0 - s y1, s y0 + c y1, y2); Rx z = (z0, ca z1 - sa z2, sa z1 + ca z2)
-  const T a0 = fma(c, in[3], -(s * in[4])), a1 = fma(s, in[3], c * in[4]), a2 = in[5];
-  const T w0 = a0, w1 = fma(ca, a1, -(sa * a2)), w2 = fma(sa, a1, ca * a2);
-  const T b0 = fma(c, in[0], -(s * in[1])), b1 = fma(s, in[0], c * in[1]), b2 = in[2];
-  const T v0 = b0, v1 = fma(ca, b1, -(sa * b2)), v2 = fma(sa, b1, ca * b2);
-  out[0] = fma(p1, w2, fma(-p2, w1, v0));
-  out[1] = fma(p2, w0, fma(-p0, w2, v1));
-  out[2] = fma(p0, w1, fma(-p1, w0, v2));
-  out[3] = w0; out[4] = w1; out[5] = w2;
+__device__ __forceinline__ void dh_ad_f(T ca, T sa, T a, T d, T s, T c, const T* in, T* out) {
+  // Tz(d): v += d e_z x w = d (-w1, w0, 0)
+  const T v0 = fma(-d, in[4], in[0]), v1 = fma(d, in[3], in[1]);
+  // Rz: (c y0 - s y1, s y0 + c y1, y2)
+  const T W0 = fma(c, in[3], -(s * in[4])), W1 = fma(s, in[3], c * in[4]);
+  T V1 = fma(s, v0, c * v1);
+  out[0] = fma(c, v0, -(s * v1));
+  // Tx(a): v += a e_x x w = a (0, -w2, w1)
+  V1 = fma(-a, in[5], V1);
+  const T V2 = fma(a, W1, in[2]);
+  // Rx: (z0, ca z1 - sa z2, sa z1 + ca z2)
+  out[1] = fma(ca, V1, -(sa * V2));
+  out[2] = fma(sa, V1, ca * V2);
+  out[3] = W0;
+  out[4] = fma(ca, W1, -(sa * in[5]));
+  out[5] = fma(sa, W1, ca * in[5]);
 }
 template <typename T>
 __device__ __forceinline__ void dh_ad_f(const LinkDH<T>& C, T s, T c, const T* in, T* out) {
-  dh_ad_f(C.ca, C.sa, C.p0, C.p1, C.p2, s, c, in, out);
+  dh_ad_f(C.ca, C.sa, C.a, C.d, s, c, in, out);
 }
 
-// (sin, cos) of theta and the variable translation of link C: revolute theta =
-// th0 + q; prismatic (PR && prism) theta = th0, p = (p0, p1 - sa q, p2 + ca q).
+// (sin, cos) of theta and the translation d of link C: revolute theta = th0 + q;
+// prismatic (PR && prism) theta = th0, d = d0 + q.
 template <bool PR, typename T>
-__device__ __forceinline__ void dh_link(const LinkDH<T>& C, bool prism, T qi, T* s, T* c, T* p1, T* p2) {
+__device__ __forceinline__ void dh_link(const LinkDH<T>& C, bool prism, T qi, T* s, T* c, T* d) {
   const T qa = (PR && prism) ? T(0) : qi;
   if (sizeof(T) == 8) {
     rd_sincos(qa + C.th0, s, c);
@@ -286,9 +306,7 @@ __device__ __forceinline__ void dh_link(const LinkDH<T>& C, bool prism, T qi, T*
     *s = fma(s0, C.cth0, c0 * C.sth0);
     *c = fma(c0, C.cth0, -(s0 * C.sth0));
   }
-  const T dq = (PR && prism) ? qi : T(0);
-  *p1 = PR ? fma(-C.sa, dq, C.p1) : C.p1;
-  *p2 = PR ? fma(C.ca, dq, C.p2) : C.p2;
+  *d = (PR && prism) ? C.d + qi : C.d;
 }
 
 // Per-state boundary vector of state b: out = A u, u = p[k*B + b] (k = 0..5).

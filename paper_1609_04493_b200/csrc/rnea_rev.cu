@@ -78,11 +78,11 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
       }
       const LinkDH<T> C = L[i];
       const bool pz = PR && PRs[i];
-      T s, c, lp1, lp2;
-      dh_link<PR>(C, pz, qi, &s, &c, &lp1, &lp2);
+      T s, c, dl;
+      dh_link<PR>(C, pz, qi, &s, &c, &dl);
       T Vn[6], Vdn[6];
-      dh_ad_finv(C.ca, C.sa, C.p0, lp1, lp2, s, c, V, Vn);
-      dh_ad_finv(C.ca, C.sa, C.p0, lp1, lp2, s, c, Vd, Vdn);
+      dh_ad_finv(C.ca, C.sa, C.a, dl, s, c, V, Vn);
+      dh_ad_finv(C.ca, C.sa, C.a, dl, s, c, Vd, Vdn);
       // S qd = (sp e_z, sr e_z); ad_V(S qd) = (sp w x e_z + sr v x e_z, sr w x e_z)
       const T sr = pz ? T(0) : qdi, sp = pz ? qdi : T(0), ar = pz ? T(0) : qai, ap = pz ? qai : T(0);
       Vn[5] += sr;
@@ -102,7 +102,7 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
     if constexpr (SB) {
       if (sb.Ft) sb_vec(sb.Ft, sb.At, B, b, F);
     }
-    T ca = 1, sa = 0, p0 = 0, p1 = 0, p2 = 0, sn = 0, cn = 1;   // child transform (identity at the tip)
+    T ca = 1, sa = 0, ac = 0, dc = 0, sn = 0, cn = 1;   // child transform (identity at the tip)
 #pragma unroll
     for (int j = 0; j < PD; ++j) {
       const int64_t o = (int64_t)max(n - 1 - j, 0) * B;
@@ -123,12 +123,12 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
       const bool pz = PR && PRs[i];
       T Fh[6], Fo[6];
       bias_force(C, V, Vd, Fh);
-      dh_bwd(ca, sa, p0, p1, p2, sn, cn, F, Fh, Fo);
+      dh_bwd(ca, sa, ac, dc, sn, cn, F, Fh, Fo);
 #pragma unroll
       for (int k = 0; k < 6; ++k) F[k] = Fo[k];
       tp = pz ? F[2] : F[5];                        // tau_i = S_i^T F_i
-      T s, c, lp1, lp2;
-      dh_link<PR>(C, pz, qi, &s, &c, &lp1, &lp2);
+      T s, c, dl;
+      dh_link<PR>(C, pz, qi, &s, &c, &dl);
       // V_{i-1}, Vdot_{i-1}
       const T sr = pz ? T(0) : qdi, sp = pz ? qdi : T(0), ar = pz ? T(0) : qai, ap = pz ? qai : T(0);
       T x[6], y[6];
@@ -141,9 +141,9 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
       y[1] = fma(sr, V[0], PR ? fma(sp, V[3], y[1]) : y[1]);
       y[3] = fma(-sr, V[4], y[3]);
       y[4] = fma(sr, V[3], y[4]);
-      dh_ad_f(C.ca, C.sa, C.p0, lp1, lp2, s, c, x, V);
-      dh_ad_f(C.ca, C.sa, C.p0, lp1, lp2, s, c, y, Vd);
-      ca = C.ca; sa = C.sa; p0 = C.p0; p1 = lp1; p2 = lp2; sn = s; cn = c;
+      dh_ad_f(C.ca, C.sa, C.a, dl, s, c, x, V);
+      dh_ad_f(C.ca, C.sa, C.a, dl, s, c, y, Vd);
+      ca = C.ca; sa = C.sa; ac = C.a; dc = dl; sn = s; cn = c;
     }
     tau[b] = tp;
   }

@@ -186,7 +186,7 @@ struct FwdState {
 template <typename T>
 struct BwdState {
   T F[6];
-  T ca, sa, p0, p1, p2, s, c;   // DH constants and stashed (sin, cos) of the child link i+1
+  T ca, sa, a, d, s, c;         // DH constants and stashed (sin, cos) of the child link i+1
   int64_t b;
   bool valid;
 #if RD_TAU_DEFER
@@ -230,7 +230,7 @@ __device__ __forceinline__ void bwd_init(BwdState<T>& g, const ThreadParams<T>& 
 #endif
 #pragma unroll
   for (int k = 0; k < 6; ++k) g.F[k] = P.bnd.Ftip[k];
-  g.ca = 1; g.sa = 0; g.p0 = g.p1 = g.p2 = 0; g.s = 0; g.c = 1;   // f_{n,n+1} = I (A5)
+  g.ca = 1; g.sa = 0; g.a = g.d = 0; g.s = 0; g.c = 1;   // f_{n,n+1} = I (A5)
 }
 // forward link k: V_k, Vdot_k, Fhat_k -> st[8]
 template <bool PR, typename T, int PD>
@@ -265,9 +265,9 @@ __device__ __forceinline__ void fwd_link(FwdState<T, PD>& f, const ThreadParams<
   T Vn[6], Vdn[6];
   if (PR) {
     const T dq = prism ? cq : T(0);
-    const T p1 = fma(-C.sa, dq, C.p1), p2 = fma(C.ca, dq, C.p2);
-    dh_ad_finv(C.ca, C.sa, C.p0, p1, p2, s, c, f.V, Vn);
-    dh_ad_finv(C.ca, C.sa, C.p0, p1, p2, s, c, f.Vd, Vdn);
+    const T dl = C.d + dq;
+    dh_ad_finv(C.ca, C.sa, C.a, dl, s, c, f.V, Vn);
+    dh_ad_finv(C.ca, C.sa, C.a, dl, s, c, f.Vd, Vdn);
     const T sr = prism ? T(0) : cqd, sp = prism ? cqd : T(0);
     const T ar = prism ? T(0) : cqa, ap = prism ? cqa : T(0);
     Vn[5] += sr;
@@ -309,7 +309,7 @@ __device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& 
   // it right after the chain stalled the warp on the fixed-latency dependency)
   if (g.valid && g.ip >= 0) tau[(int64_t)g.ip * B + g.b] = g.tp;
 #endif
-  dh_bwd(g.ca, g.sa, g.p0, g.p1, g.p2, g.s, g.c, g.F, cur + 2, Fo);
+  dh_bwd(g.ca, g.sa, g.a, g.d, g.s, g.c, g.F, cur + 2, Fo);
 #pragma unroll
   for (int j = 0; j < 6; ++j) g.F[j] = Fo[j];
   const LinkDH<T>& C = P.L[i];
@@ -321,14 +321,12 @@ __device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& 
 #else
   if (g.valid) tau[(int64_t)i * B + g.b] = ti;
 #endif
-  g.ca = C.ca; g.sa = C.sa; g.p0 = C.p0;
+  g.ca = C.ca; g.sa = C.sa; g.a = C.a;
   if (PR) {
-    const T dq = prism ? cur[0] : T(0);
-    g.p1 = fma(-C.sa, dq, C.p1);
-    g.p2 = fma(C.ca, dq, C.p2);
+    g.d = prism ? C.d + cur[0] : C.d;               // prismatic: d = d0 + q
     g.s = prism ? C.sth0 : cur[0];
   } else {
-    g.p1 = C.p1; g.p2 = C.p2;
+    g.d = C.d;
     g.s = cur[0];
   }
   g.c = cur[1];
