@@ -269,16 +269,16 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
         for (int k = 0; k < 6; ++k) V[k] = Vn[k];
       }
     }
-    Sym6<T> K, Kc;
+    Sym6<T> K;                                            // carried X^T Jhat^a X (0 at the tip)
     T pc[6];
     int fail = 0;                                         // tip-most link with Omega <= 0 (1-based)
 #pragma unroll
-    for (int k = 0; k < 6; ++k) { pc[k] = bnd.Ftip[k]; Kc.a[k] = 0; Kc.c[k] = 0; }
+    for (int k = 0; k < 6; ++k) { pc[k] = bnd.Ftip[k]; K.a[k] = 0; K.c[k] = 0; }
     if constexpr (SB) {
       if (sb.Ft) sb_vec(sb.Ft, sb.At, B, b, pc);
     }
 #pragma unroll
-    for (int k = 0; k < 9; ++k) Kc.b[k] = 0;
+    for (int k = 0; k < 9; ++k) K.b[k] = 0;
     // sweep 2 (backward); inputs one link ahead (each iteration is long)
     T cq = __ldg(pq + (int64_t)(n - 1) * B), cqd = __ldg(pqd + (int64_t)(n - 1) * B),
       ct = __ldg(pt + (int64_t)(n - 1) * B);
@@ -302,12 +302,8 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
         cc[0] = qdi * V[1]; cc[1] = -qdi * V[0]; cc[2] = 0; cc[3] = qdi * V[4]; cc[4] = -qdi * V[3]; cc[5] = 0;
       }
       T ph[6];
-      bias_force(C, V, zero6, ph);
-      dh_inertia(C, K);
-#pragma unroll
-      for (int k = 0; k < 6; ++k) { K.a[k] += Kc.a[k]; K.c[k] += Kc.c[k]; ph[k] += pc[k]; }
-#pragma unroll
-      for (int k = 0; k < 9; ++k) K.b[k] += Kc.b[k];
+      bias_force_v(C, V, pc, ph);                         // phat_i = p_i + X^T p^a_{i+1}
+      sym6_add_inertia(C, K);                             // Jhat_i = J_i + X^T Jhat^a_{i+1} X
       // revolute: U = K e_5 = (B[:, 2], C[:, 2]); prismatic: U = K e_2 = (A[:, 2], B[2, :])
       T U[6] = {K.b[2], K.b[5], K.b[8], K.c[4], K.c[5], K.c[2]};
       if (PR && pz) {
@@ -323,17 +319,16 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
       for (int k = 0; k < 6; ++k) w[k * slots] = U[k] * invD;
       w[6 * slots] = ub;
       if (i > 0) {
-        sym6_rank1_sub(K, U, invD);
-        T Kcc[6], pa[6];
-        sym6_mv(K, cc, Kcc);
+        sym6_rank1_sub(K, U, invD);                       // Jhat^a
+        T y0[6], pa[6];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) pa[k] = ph[k] + Kcc[k] + U[k] * ub;
-        Kc = K;
+        for (int k = 0; k < 6; ++k) y0[k] = fma(U[k], ub, ph[k]);
+        sym6_mv_xy(K, cc, y0, pa);                        // p^a = phat + Jhat^a c + U u / D
         if constexpr (PR) {
-          dh_congruence(C.ca, C.sa, C.a, dl, s, c, Kc);
+          dh_congruence(C.ca, C.sa, C.a, dl, s, c, K);
           dh_bwd(C.ca, C.sa, C.a, dl, s, c, pa, zero6, pc);
         } else {
-          dh_congruence(C, s, c, Kc);
+          dh_congruence(C, s, c, K);
           dh_bwd(C.ca, C.sa, C.a, C.d, s, c, pa, zero6, pc);
         }
         T x[6];

@@ -230,6 +230,35 @@ __device__ __forceinline__ void dh_congruence(const LinkDH<T>& C, T s, T c, Sym6
   dh_congruence(C.ca, C.sa, C.a, C.d, s, c, K);
 }
 
+// K += J for the link inertia J = [[m I, -[h]], [[h], I]]: only its 15 structural
+// non-zeros are added.
+template <typename T, typename CT>
+__device__ __forceinline__ void sym6_add_inertia(const CT& C, Sym6<T>& K) {
+  K.a[0] += C.m; K.a[1] += C.m; K.a[2] += C.m;
+  const T h0 = C.h[0], h1 = C.h[1], h2 = C.h[2];
+  K.b[1] += h2;  K.b[2] -= h1;
+  K.b[3] -= h2;  K.b[5] += h0;
+  K.b[6] += h1;  K.b[7] -= h0;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) K.c[k] += C.I[k];
+}
+
+// y = y0 + K x for x with x[2] = x[5] = 0 (the ABA's c_i = ad_V(S qd), S = e_z or
+// e_5), y0 seeding the chains.
+template <typename T>
+__device__ __forceinline__ void sym6_mv_xy(const Sym6<T>& K, const T* x, const T* y0, T* y) {
+  const T* A = K.a;
+  const T* Bm = K.b;
+  const T* C = K.c;
+  const T x0 = x[0], x1 = x[1], x3 = x[3], x4 = x[4];
+  y[0] = fma(A[0], x0, fma(A[3], x1, fma(Bm[0], x3, fma(Bm[1], x4, y0[0]))));
+  y[1] = fma(A[3], x0, fma(A[1], x1, fma(Bm[3], x3, fma(Bm[4], x4, y0[1]))));
+  y[2] = fma(A[4], x0, fma(A[5], x1, fma(Bm[6], x3, fma(Bm[7], x4, y0[2]))));
+  y[3] = fma(Bm[0], x0, fma(Bm[3], x1, fma(C[0], x3, fma(C[3], x4, y0[3]))));
+  y[4] = fma(Bm[1], x0, fma(Bm[4], x1, fma(C[3], x3, fma(C[1], x4, y0[4]))));
+  y[5] = fma(Bm[2], x0, fma(Bm[5], x1, fma(C[4], x3, fma(C[5], x4, y0[5]))));
+}
+
 template <typename T>
 __device__ __forceinline__ void dh_inertia(const LinkDH<T>& C, Sym6<T>& K) {
   K.a[0] = C.m; K.a[1] = C.m; K.a[2] = C.m; K.a[3] = 0; K.a[4] = 0; K.a[5] = 0;

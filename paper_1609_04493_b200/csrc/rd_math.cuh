@@ -168,6 +168,29 @@ __device__ __forceinline__ void bias_force(const CT& C, const T* V, const T* Vd,
   Fh[5] = fma(v0, Pf1, fma(-v1, Pf0, fma(w0, Pm1, fma(-w1, Pm0, Am2))));
 }
 
+// Fh = Pc - ad^T_V (J V) = Pc + (w x P_f, v x P_f + w x P_m), P = J V: the bias
+// wrench of a link with Vdot = 0 (the ABA's p_i) plus the wrench Pc
+// carried from the child, Pc seeding the FMA chains (42 FP64 instructions; the
+// general bias_force with a zero Vdot would spend 24 more on J 0).
+template <typename T, typename CT>
+__device__ __forceinline__ void bias_force_v(const CT& C, const T* V, const T* Pc, T* Fh) {
+  const T m = C.m, h0 = C.h[0], h1 = C.h[1], h2 = C.h[2];
+  const T Ixx = C.I[0], Iyy = C.I[1], Izz = C.I[2], Ixy = C.I[3], Ixz = C.I[4], Iyz = C.I[5];
+  const T Pf0 = fma(m, V[0], fma(-h1, V[5], h2 * V[4]));
+  const T Pf1 = fma(m, V[1], fma(-h2, V[3], h0 * V[5]));
+  const T Pf2 = fma(m, V[2], fma(-h0, V[4], h1 * V[3]));
+  const T Pm0 = fma(h1, V[2], fma(-h2, V[1], fma(Ixx, V[3], fma(Ixy, V[4], Ixz * V[5]))));
+  const T Pm1 = fma(h2, V[0], fma(-h0, V[2], fma(Ixy, V[3], fma(Iyy, V[4], Iyz * V[5]))));
+  const T Pm2 = fma(h0, V[1], fma(-h1, V[0], fma(Ixz, V[3], fma(Iyz, V[4], Izz * V[5]))));
+  const T w0 = V[3], w1 = V[4], w2 = V[5], v0 = V[0], v1 = V[1], v2 = V[2];
+  Fh[0] = fma(w1, Pf2, fma(-w2, Pf1, Pc[0]));
+  Fh[1] = fma(w2, Pf0, fma(-w0, Pf2, Pc[1]));
+  Fh[2] = fma(w0, Pf1, fma(-w1, Pf0, Pc[2]));
+  Fh[3] = fma(v1, Pf2, fma(-v2, Pf1, fma(w1, Pm2, fma(-w2, Pm1, Pc[3]))));
+  Fh[4] = fma(v2, Pf0, fma(-v0, Pf2, fma(w2, Pm0, fma(-w0, Pm2, Pc[4]))));
+  Fh[5] = fma(v0, Pf1, fma(-v1, Pf0, fma(w0, Pm1, fma(-w1, Pm0, Pc[5]))));
+}
+
 // One forward step of Eq. (1) for link with constants C:
 //   V  = Ad_{f^-1} Vp + S qd
 //   Vd = Ad_{f^-1} Vdp + S qdd + ad_V (S qd)      (= ... - ad_{S qd} Ad_{f^-1} Vp)
