@@ -394,7 +394,9 @@ def main():
         "gpu_launches": launches,
         "e2e": e2e,
     }
-    if not args.no_cpu_baseline and fd:
+    if world > 1:
+        pass                                        # the CPU baseline is an N = 1 figure (rank 0 only)
+    elif not args.no_cpu_baseline and fd:
         line["cpu_baseline"] = cpu_baseline_fd(robot, g, cfg, n, args.cpu_seconds)
     elif not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(robot, g, cfg, n, args.cpu_seconds)
