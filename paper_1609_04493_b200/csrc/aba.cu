@@ -40,7 +40,7 @@ namespace rd {
 #define RD_ABA_S1U 4
 #endif
 #ifndef RD_ABA_S3PD
-#define RD_ABA_S3PD 1
+#define RD_ABA_S3PD 2          // re-measured after the sweep-2 trim: 2 / 2 0.4578 vs 1 / 2 0.4604 ms (C4)
 #endif
 #ifndef RD_ABA_S3U
 #define RD_ABA_S3U 2
