@@ -152,6 +152,8 @@ struct rd_model_s {
   std::vector<rd::LinkDH<float>> D32;
   rd::LinkDH<double>* dD64 = nullptr;
   rd::LinkDH<float>* dD32 = nullptr;
+  std::vector<rd::LinkDHc<double>> C64;   // thread kernel: the same frames, inertia about the CoM
+  std::vector<rd::LinkDHc<float>> C32;
   Rigid D0;                        // DH base frame in the user's base frame
   rd::Boundary<double> bdh64;
   rd::Boundary<float> bdh32;
@@ -274,6 +276,8 @@ bool build_dh(rd_model_t m, const std::vector<Rigid>& Mp, const std::vector<std:
   m->D0 = D[0];
   m->D64.resize(n);
   m->D32.resize(n);
+  m->C64.resize(n);
+  m->C32.resize(n);
   for (int i = 0; i < n; ++i) {
     const Rigid Mi = (i == 0) ? rigid_identity() : rigid_mul(rigid_inv(D[i - 1]), D[i]);
     const double ca = Mi.R[2][2], sa = -Mi.R[1][2];
@@ -317,6 +321,23 @@ bool build_dh(rd_model_t m, const std::vector<Rigid>& Mp, const std::vector<std:
     F.cth0 = (float)L.cth0; F.sth0 = (float)L.sth0;
     for (int k = 0; k < 3; ++k) F.h[k] = (float)L.h[k];
     for (int k = 0; k < 6; ++k) F.I[k] = (float)L.I[k];
+    // inertia about the centre of mass c = h / m: I_c = I - m (|c|^2 1 - c c^T)
+    rd::LinkDHc<double>& Lc = m->C64[i];
+    Lc.ca = L.ca; Lc.sa = L.sa; Lc.a = L.a; Lc.d = L.d;
+    Lc.th0 = L.th0; Lc.cth0 = L.cth0; Lc.sth0 = L.sth0; Lc.m = L.m;
+    for (int k = 0; k < 3; ++k) Lc.c[k] = L.h[k] / L.m;
+    const double c2 = Lc.c[0] * Lc.c[0] + Lc.c[1] * Lc.c[1] + Lc.c[2] * Lc.c[2];
+    Lc.Ic[0] = L.I[0] - L.m * (c2 - Lc.c[0] * Lc.c[0]);
+    Lc.Ic[1] = L.I[1] - L.m * (c2 - Lc.c[1] * Lc.c[1]);
+    Lc.Ic[2] = L.I[2] - L.m * (c2 - Lc.c[2] * Lc.c[2]);
+    Lc.Ic[3] = L.I[3] + L.m * Lc.c[0] * Lc.c[1];
+    Lc.Ic[4] = L.I[4] + L.m * Lc.c[0] * Lc.c[2];
+    Lc.Ic[5] = L.I[5] + L.m * Lc.c[1] * Lc.c[2];
+    rd::LinkDHc<float>& Fc = m->C32[i];
+    Fc.ca = (float)Lc.ca; Fc.sa = (float)Lc.sa; Fc.a = (float)Lc.a; Fc.d = (float)Lc.d;
+    Fc.th0 = (float)Lc.th0; Fc.cth0 = (float)Lc.cth0; Fc.sth0 = (float)Lc.sth0; Fc.m = (float)Lc.m;
+    for (int k = 0; k < 3; ++k) Fc.c[k] = (float)Lc.c[k];
+    for (int k = 0; k < 6; ++k) Fc.Ic[k] = (float)Lc.Ic[k];
   }
   return true;
 }
@@ -388,6 +409,9 @@ template <> const rd::LinkConst<float>* dev_consts<float>(rd_model_t m) { return
 template <typename T> const rd::LinkDH<T>* dh_consts(rd_model_t m);
 template <> const rd::LinkDH<double>* dh_consts<double>(rd_model_t m) { return m->D64.data(); }
 template <> const rd::LinkDH<float>* dh_consts<float>(rd_model_t m) { return m->D32.data(); }
+template <typename T> const rd::LinkDHc<T>* dhc_consts(rd_model_t m);
+template <> const rd::LinkDHc<double>* dhc_consts<double>(rd_model_t m) { return m->C64.data(); }
+template <> const rd::LinkDHc<float>* dhc_consts<float>(rd_model_t m) { return m->C32.data(); }
 template <typename T> const rd::LinkDH<T>* dh_dev(rd_model_t m);
 template <> const rd::LinkDH<double>* dh_dev<double>(rd_model_t m) { return m->dD64; }
 template <> const rd::LinkDH<float>* dh_dev<float>(rd_model_t m) { return m->dD32; }
@@ -501,7 +525,7 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   cudaError_t e = cudaSuccess;
   if (strat == RD_STRAT_THREAD) {
     bool ok = false;
-    e = rd::launch_rnea_thread<T>(m->n, dh_consts<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok,
+    e = rd::launch_rnea_thread<T>(m->n, dhc_consts<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok,
                                   m->prism_mask, pd);
     if (!ok) strat = m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
   } else if (strat == RD_STRAT_WARP_SCAN) {

@@ -42,6 +42,20 @@ struct LinkDH {
   T I[6];
 };
 
+// The thread kernel's per-link constants: the DH transform of LinkDH and the
+// inertia about the centre of mass (for the Newton-Euler form of Fhat,
+// rd_math.cuh bias_force_com): c = h / m, I_c = I - m (|c|^2 1 - c c^T).
+template <typename T>
+struct LinkDHc {
+  T ca, sa;
+  T a, d;
+  T th0;
+  T cth0, sth0;
+  T m;
+  T c[3];         // centre of mass in the DH frame
+  T Ic[6];        // rotational inertia about the centre of mass (xx yy zz xy xz yz)
+};
+
 // Boundary data of Eq. (3) in the joint frames: V_0, Vdot_0 (base frame,
 // unchanged) and F_{n+1} (expressed in link n's joint frame).
 template <typename T>
@@ -88,7 +102,7 @@ enum Strategy { kAuto = 0, kThread = 1, kWarpScan = 2, kGeneric = 3 };
 // non-positive Cholesky pivot).
 // prism_mask: bit i set = link i prismatic (DH kernels; n <= 32 here).
 template <typename T>
-cudaError_t launch_rnea_thread(int n, const LinkDH<T>* L_host, const Boundary<T>& bnd,
+cudaError_t launch_rnea_thread(int n, const LinkDHc<T>* L_host, const Boundary<T>& bnd,
                                int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
                                cudaStream_t st, int* launches, bool* supported, uint32_t prism_mask = 0,
                                const StateBoundary<T>* sb = nullptr);

@@ -168,6 +168,35 @@ __device__ __forceinline__ void bias_force(const CT& C, const T* V, const T* Vd,
   Fh[5] = fma(v0, Pf1, fma(-v1, Pf0, fma(w0, Pm1, fma(-w1, Pm0, Am2))));
 }
 
+// Fhat = J Vd - ad^T_V (J V) evaluated at the centre of mass c, where J
+// is block diagonal (Newton-Euler form; C: LinkDHc):
+//   v_c = v + w x c,  a_c = vd + wd x c,  f = m (a_c + w x v_c),
+//   n_c = I_c wd + w x (I_c w),  Fhat = (f, n_c + c x f)
+// 51 FP64 instructions instead of the 66 of bias_force.
+template <typename T, typename CT>
+__device__ __forceinline__ void bias_force_com(const CT& C, const T* V, const T* Vd, T* Fh) {
+  const T c0 = C.c[0], c1 = C.c[1], c2 = C.c[2];
+  const T w0 = V[3], w1 = V[4], w2 = V[5];
+  const T dw0 = Vd[3], dw1 = Vd[4], dw2 = Vd[5];
+  const T vc0 = fma(w1, c2, fma(-w2, c1, V[0]));
+  const T vc1 = fma(w2, c0, fma(-w0, c2, V[1]));
+  const T vc2 = fma(w0, c1, fma(-w1, c0, V[2]));
+  const T ac0 = fma(dw1, c2, fma(-dw2, c1, Vd[0]));
+  const T ac1 = fma(dw2, c0, fma(-dw0, c2, Vd[1]));
+  const T ac2 = fma(dw0, c1, fma(-dw1, c0, Vd[2]));
+  const T f0 = C.m * fma(w1, vc2, fma(-w2, vc1, ac0));
+  const T f1 = C.m * fma(w2, vc0, fma(-w0, vc2, ac1));
+  const T f2 = C.m * fma(w0, vc1, fma(-w1, vc0, ac2));
+  const T Ixx = C.Ic[0], Iyy = C.Ic[1], Izz = C.Ic[2], Ixy = C.Ic[3], Ixz = C.Ic[4], Iyz = C.Ic[5];
+  const T L0 = fma(Ixx, w0, fma(Ixy, w1, Ixz * w2));
+  const T L1 = fma(Ixy, w0, fma(Iyy, w1, Iyz * w2));
+  const T L2 = fma(Ixz, w0, fma(Iyz, w1, Izz * w2));
+  Fh[0] = f0; Fh[1] = f1; Fh[2] = f2;
+  Fh[3] = fma(c1, f2, fma(-c2, f1, fma(w1, L2, fma(-w2, L1, fma(Ixx, dw0, fma(Ixy, dw1, Ixz * dw2))))));
+  Fh[4] = fma(c2, f0, fma(-c0, f2, fma(w2, L0, fma(-w0, L2, fma(Ixy, dw0, fma(Iyy, dw1, Iyz * dw2))))));
+  Fh[5] = fma(c0, f1, fma(-c1, f0, fma(w0, L1, fma(-w1, L0, fma(Ixz, dw0, fma(Iyz, dw1, Izz * dw2))))));
+}
+
 // Fh = Pc - ad^T_V (J V) = Pc + (w x P_f, v x P_f + w x P_m), P = J V: the bias
 // wrench of a link with Vdot = 0 (the ABA's p_i) plus the wrench Pc
 // carried from the child, Pc seeding the FMA chains (42 FP64 instructions; the
@@ -263,8 +292,8 @@ __device__ __forceinline__ void dh_ad_finv(T ca, T sa, T a, T d, T s, T c, const
   out[2] = v2;
   out[3] = W0; out[4] = W1; out[5] = w2;
 }
-template <typename T>
-__device__ __forceinline__ void dh_ad_finv(const LinkDH<T>& C, T s, T c, const T* in, T* out) {
+template <typename T, typename CT>
+__device__ __forceinline__ void dh_ad_finv(const CT& C, T s, T c, const T* in, T* out) {
   dh_ad_finv(C.ca, C.sa, C.a, C.d, s, c, in, out);
 }
 

@@ -33,7 +33,7 @@ constexpr int kMaxThreadN = 32;
 
 template <typename T>
 struct ThreadParams {
-  LinkDH<T> L[kMaxThreadN];
+  LinkDHc<T> L[kMaxThreadN];   // DH transform + inertia about the CoM
   Boundary<T> bnd;
   int n;          // links
   int lt;         // links stashed in TMEM (the rest in shared memory)
@@ -247,7 +247,7 @@ __device__ __forceinline__ void fwd_link(FwdState<T, PD>& f, const ThreadParams<
   const T f_q = __ldg((here ? f.pq : f.xq) + off2);
   const T f_qd = __ldg((here ? f.pqd : f.xqd) + off2);
   const T f_qa = __ldg((here ? f.pqa : f.xqa) + off2);
-  const LinkDH<T>& C = P.L[k];
+  const LinkDHc<T>& C = P.L[k];
   // PR (the model has prismatic joints): link type from C.pr (warp-uniform), selects only.
   const bool prism = PR && ((P.prism >> k) & 1u);
   const T qang = prism ? T(0) : cq;               // revolute: theta = th0 + q; prismatic: th0
@@ -292,7 +292,7 @@ __device__ __forceinline__ void fwd_link(FwdState<T, PD>& f, const ThreadParams<
     st[0] = s;
   }
   st[1] = c;
-  bias_force(C, Vn, Vdn, st + 2);
+  bias_force_com(C, Vn, Vdn, st + 2);
 #pragma unroll
   for (int j = 0; j < 6; ++j) { f.V[j] = Vn[j]; f.Vd[j] = Vdn[j]; }
 #pragma unroll
@@ -312,7 +312,7 @@ __device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& 
   dh_bwd(g.ca, g.sa, g.a, g.d, g.s, g.c, g.F, cur + 2, Fo);
 #pragma unroll
   for (int j = 0; j < 6; ++j) g.F[j] = Fo[j];
-  const LinkDH<T>& C = P.L[i];
+  const LinkDHc<T>& C = P.L[i];
   const bool prism = PR && ((P.prism >> i) & 1u);
   const T ti = prism ? g.F[2] : g.F[5];            // tau_i = S_i^T F_i
 #if RD_TAU_DEFER
@@ -574,7 +574,7 @@ static cudaError_t launch_w(const ThreadParams<T>& P, size_t smem, int64_t B, co
 }
 
 template <typename T>
-cudaError_t launch_rnea_thread(int n, const LinkDH<T>* L_host, const Boundary<T>& bnd, int64_t B,
+cudaError_t launch_rnea_thread(int n, const LinkDHc<T>* L_host, const Boundary<T>& bnd, int64_t B,
                                const T* q, const T* qd, const T* qdd, T* tau, cudaStream_t st,
                                int* launches, bool* supported, uint32_t prism_mask, const StateBoundary<T>* sb) {
   StashPlan plan;
@@ -604,10 +604,10 @@ cudaError_t launch_rnea_thread(int n, const LinkDH<T>* L_host, const Boundary<T>
   return launch_w<T, 8, false, false>(P, plan.smem, B, q, qd, qdd, tau, st, nsb);
 }
 
-template cudaError_t launch_rnea_thread<double>(int, const LinkDH<double>*, const Boundary<double>&, int64_t,
+template cudaError_t launch_rnea_thread<double>(int, const LinkDHc<double>*, const Boundary<double>&, int64_t,
                                                 const double*, const double*, const double*, double*,
                                                 cudaStream_t, int*, bool*, uint32_t, const StateBoundary<double>*);
-template cudaError_t launch_rnea_thread<float>(int, const LinkDH<float>*, const Boundary<float>&, int64_t,
+template cudaError_t launch_rnea_thread<float>(int, const LinkDHc<float>*, const Boundary<float>&, int64_t,
                                                const float*, const float*, const float*, float*,
                                                cudaStream_t, int*, bool*, uint32_t, const StateBoundary<float>*);
 
