@@ -154,6 +154,8 @@ struct rd_model_s {
   rd::LinkDH<float>* dD32 = nullptr;
   std::vector<rd::LinkDHc<double>> C64;   // thread kernel: the same frames, inertia about the CoM
   std::vector<rd::LinkDHc<float>> C32;
+  rd::LinkDHc<double>* dC64 = nullptr;   // device copies (REVERSE kernel)
+  rd::LinkDHc<float>* dC32 = nullptr;
   Rigid D0;                        // DH base frame in the user's base frame
   rd::Boundary<double> bdh64;
   rd::Boundary<float> bdh32;
@@ -412,6 +414,9 @@ template <> const rd::LinkDH<float>* dh_consts<float>(rd_model_t m) { return m->
 template <typename T> const rd::LinkDHc<T>* dhc_consts(rd_model_t m);
 template <> const rd::LinkDHc<double>* dhc_consts<double>(rd_model_t m) { return m->C64.data(); }
 template <> const rd::LinkDHc<float>* dhc_consts<float>(rd_model_t m) { return m->C32.data(); }
+template <typename T> const rd::LinkDHc<T>* dhc_dev(rd_model_t m);
+template <> const rd::LinkDHc<double>* dhc_dev<double>(rd_model_t m) { return m->dC64; }
+template <> const rd::LinkDHc<float>* dhc_dev<float>(rd_model_t m) { return m->dC32; }
 template <typename T> const rd::LinkDH<T>* dh_dev(rd_model_t m);
 template <> const rd::LinkDH<double>* dh_dev<double>(rd_model_t m) { return m->dD64; }
 template <> const rd::LinkDH<float>* dh_dev<float>(rd_model_t m) { return m->dD32; }
@@ -550,7 +555,7 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     if (!ok) strat = RD_STRAT_GENERIC;
   }
   if (strat == RD_STRAT_REVERSE) {
-    e = rd::launch_rnea_rev<T>(m->n, dh_dev<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches,
+    e = rd::launch_rnea_rev<T>(m->n, dhc_dev<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches,
                                m->has_prism ? m->dPrism : nullptr, pd);
   }
   if (strat == RD_STRAT_GENERIC) {
@@ -811,6 +816,10 @@ rd_status_t rd_model_create(int32_t n, const double* M, const double* S, const d
     if (e == cudaSuccess) e = cudaMalloc(&m->dD32, sizeof(rd::LinkDH<float>) * n);
     if (e == cudaSuccess) e = cudaMemcpy(m->dD64, m->D64.data(), sizeof(rd::LinkDH<double>) * n, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(m->dD32, m->D32.data(), sizeof(rd::LinkDH<float>) * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&m->dC64, sizeof(rd::LinkDHc<double>) * n);
+    if (e == cudaSuccess) e = cudaMalloc(&m->dC32, sizeof(rd::LinkDHc<float>) * n);
+    if (e == cudaSuccess) e = cudaMemcpy(m->dC64, m->C64.data(), sizeof(rd::LinkDHc<double>) * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(m->dC32, m->C32.data(), sizeof(rd::LinkDHc<float>) * n, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && m->has_prism) e = cudaMalloc(&m->dPrism, n);
     if (e == cudaSuccess && m->has_prism) e = cudaMemcpy(m->dPrism, m->prism.data(), n, cudaMemcpyHostToDevice);
   }
@@ -828,6 +837,8 @@ rd_status_t rd_model_destroy(rd_model_t m) {
   if (m->dL32) cudaFree(m->dL32);
   if (m->dD64) cudaFree(m->dD64);
   if (m->dD32) cudaFree(m->dD32);
+  if (m->dC64) cudaFree(m->dC64);
+  if (m->dC32) cudaFree(m->dC32);
   if (m->dPrism) cudaFree(m->dPrism);
   if (m->ws) cudaFree(m->ws);
   for (int k = 0; k < 2; ++k) {

@@ -42,7 +42,7 @@ struct LinkDH {
   T I[6];
 };
 
-// The thread kernel's per-link constants: the DH transform of LinkDH and the
+// The thread and REVERSE kernels' per-link constants: the DH transform of LinkDH and the
 // inertia about the centre of mass (for the Newton-Euler form of Fhat,
 // rd_math.cuh bias_force_com): c = h / m, I_c = I - m (|c|^2 1 - c c^T).
 template <typename T>
@@ -138,7 +138,7 @@ cudaError_t launch_rnea_block(int n, const LinkConst<T>* L_dev, const Boundary<T
                               cudaStream_t st, int* launches, bool* supported);
 // prism: device uint8[n], 1 = prismatic link (nullptr: all revolute).
 template <typename T>
-cudaError_t launch_rnea_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd,
+cudaError_t launch_rnea_rev(int n, const LinkDHc<T>* L_dev, const Boundary<T>& bnd,
                             int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
                             cudaStream_t st, int* launches, const unsigned char* prism = nullptr,
                             const StateBoundary<T>* sb = nullptr);

@@ -347,8 +347,8 @@ __device__ __forceinline__ void dh_ad_f(const LinkDH<T>& C, T s, T c, const T* i
 
 // (sin, cos) of theta and the translation d of link C: revolute theta = th0 + q;
 // prismatic (PR && prism) theta = th0, d = d0 + q.
-template <bool PR, typename T>
-__device__ __forceinline__ void dh_link(const LinkDH<T>& C, bool prism, T qi, T* s, T* c, T* d) {
+template <bool PR, typename T, typename CT>
+__device__ __forceinline__ void dh_link(const CT& C, bool prism, T qi, T* s, T* c, T* d) {
   const T qa = (PR && prism) ? T(0) : qi;
   if (sizeof(T) == 8) {
     rd_sincos(qa + C.th0, s, c);

@@ -36,14 +36,14 @@ constexpr int kRevPD = RD_REV_PD, kRevU = RD_REV_U;
 
 template <typename T, bool PR, bool SB>
 __global__ void __launch_bounds__(kRevThreads, RD_REV_MB)
-rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
+rnea_rev_kernel(int n, const LinkDHc<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
                 const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
                 T* __restrict__ tau, const unsigned char* __restrict__ prism_g,
                 const typename SBArg<T, SB>::type sb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LinkDH<T>* L = reinterpret_cast<LinkDH<T>*>(smem_raw);       // model constants, broadcast reads
-  unsigned char* PRs = smem_raw + (size_t)n * sizeof(LinkDH<T>);   // prismatic flags (PR only)
-  for (int i = threadIdx.x; i < n * (int)(sizeof(LinkDH<T>) / sizeof(T)); i += blockDim.x)
+  LinkDHc<T>* L = reinterpret_cast<LinkDHc<T>*>(smem_raw);       // model constants, broadcast reads
+  unsigned char* PRs = smem_raw + (size_t)n * sizeof(LinkDHc<T>);   // prismatic flags (PR only)
+  for (int i = threadIdx.x; i < n * (int)(sizeof(LinkDHc<T>) / sizeof(T)); i += blockDim.x)
     reinterpret_cast<T*>(L)[i] = reinterpret_cast<const T*>(Lg)[i];
   if (PR)
     for (int i = threadIdx.x; i < n; i += blockDim.x) PRs[i] = prism_g[i];
@@ -76,7 +76,7 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
         const int64_t o = (int64_t)min(i + PD, n - 1) * B;
         aq[PD - 1] = __ldg(pq + o); aqd[PD - 1] = __ldg(pqd + o); aqa[PD - 1] = __ldg(pqa + o);
       }
-      const LinkDH<T> C = L[i];
+      const LinkDHc<T> C = L[i];
       const bool pz = PR && PRs[i];
       T s, c, dl;
       dh_link<PR>(C, pz, qi, &s, &c, &dl);
@@ -119,10 +119,10 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
         aq[PD - 1] = __ldg(pq + o); aqd[PD - 1] = __ldg(pqd + o); aqa[PD - 1] = __ldg(pqa + o);
       }
       if (i < n - 1) tau[(int64_t)(i + 1) * B + b] = tp;
-      const LinkDH<T> C = L[i];
+      const LinkDHc<T> C = L[i];
       const bool pz = PR && PRs[i];
       T Fh[6], Fo[6];
-      bias_force(C, V, Vd, Fh);
+      bias_force_com(C, V, Vd, Fh);
       dh_bwd(ca, sa, ac, dc, sn, cn, F, Fh, Fo);
 #pragma unroll
       for (int k = 0; k < 6; ++k) F[k] = Fo[k];
@@ -150,10 +150,10 @@ rnea_rev_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, 
 }
 
 template <typename T, bool PR, bool SB>
-static cudaError_t launch_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
+static cudaError_t launch_rev(int n, const LinkDHc<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                               const T* qd, const T* qdd, T* tau, cudaStream_t st, const unsigned char* prism,
                               const typename SBArg<T, SB>::type& sb) {
-  const size_t smem = (size_t)n * sizeof(LinkDH<T>) + (PR ? (size_t)n : 0);
+  const size_t smem = (size_t)n * sizeof(LinkDHc<T>) + (PR ? (size_t)n : 0);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(rnea_rev_kernel<T, PR, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
@@ -168,7 +168,7 @@ static cudaError_t launch_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& 
 }
 
 template <typename T>
-cudaError_t launch_rnea_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
+cudaError_t launch_rnea_rev(int n, const LinkDHc<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
                             const T* qd, const T* qdd, T* tau, cudaStream_t st, int* launches,
                             const unsigned char* prism, const StateBoundary<T>* sb) {
   ++*launches;
@@ -179,10 +179,10 @@ cudaError_t launch_rnea_rev(int n, const LinkDH<T>* L_dev, const Boundary<T>& bn
                : launch_rev<T, false, false>(n, L_dev, bnd, B, q, qd, qdd, tau, st, nullptr, NoStateBoundary{});
 }
 
-template cudaError_t launch_rnea_rev<double>(int, const LinkDH<double>*, const Boundary<double>&, int64_t,
+template cudaError_t launch_rnea_rev<double>(int, const LinkDHc<double>*, const Boundary<double>&, int64_t,
                                              const double*, const double*, const double*, double*, cudaStream_t,
                                              int*, const unsigned char*, const StateBoundary<double>*);
-template cudaError_t launch_rnea_rev<float>(int, const LinkDH<float>*, const Boundary<float>&, int64_t,
+template cudaError_t launch_rnea_rev<float>(int, const LinkDHc<float>*, const Boundary<float>&, int64_t,
                                             const float*, const float*, const float*, float*, cudaStream_t, int*,
                                             const unsigned char*, const StateBoundary<float>*);
 
