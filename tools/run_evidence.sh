@@ -20,4 +20,5 @@ bash tools/run_ncu_one.sh warp_C3_f64 rnea_warp_kernel --strategy warp_scan --ba
 timeout 2400 python tools/sweep.py > $R/sweep_f64.csv 2> $R/sweep_f64.err
 timeout 900 python tools/sweep.py --dtype f32 --fd-n 10,30 --cpu-seconds 1 > $R/sweep_f32.csv 2> $R/sweep_f32.err
 timeout 600 python tools/latency.py > $R/latency.csv 2>&1
+timeout 300 python tools/small_probe.py C2 C3 > $R/small_probe.csv 2>&1
 ls -la $R gpurun_out/ncu
