@@ -319,16 +319,17 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
       for (int k = 0; k < 6; ++k) w[k * slots] = U[k] * invD;
       w[6 * slots] = ub;
       if (i > 0) {
-        sym6_rank1_sub(K, U, invD);                       // Jhat^a
+        if constexpr (PR) sym6_rank1_sub(K, U, invD);     // Jhat^a
+        else sym6_rank1_sub_rev(K, U, invD);
         T y0[6], pa[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) y0[k] = fma(U[k], ub, ph[k]);
-        sym6_mv_xy(K, cc, y0, pa);                        // p^a = phat + Jhat^a c + U u / D
+        sym6_mv_xy<T, !PR>(K, cc, y0, pa);                // p^a = phat + Jhat^a c + U u / D
         if constexpr (PR) {
           dh_congruence(C.ca, C.sa, C.a, dl, s, c, K);
           dh_bwd(C.ca, C.sa, C.a, dl, s, c, pa, zero6, pc);
         } else {
-          dh_congruence(C, s, c, K);
+          dh_congruence_rev(C.ca, C.sa, C.a, C.d, s, c, K);
           dh_bwd(C.ca, C.sa, C.a, C.d, s, c, pa, zero6, pc);
         }
         T x[6];

@@ -230,6 +230,84 @@ __device__ __forceinline__ void dh_congruence(const LinkDH<T>& C, T s, T c, Sym6
   dh_congruence(C.ca, C.sa, C.a, C.d, s, c, K);
 }
 
+// Revolute joint in DH frames, S = e_5, U = K e_5, D = U_5: Jhat^a = K - U U^T / D has
+// row and column 5 identically zero (Jhat^a S = U - U D / D = 0).  The rank-1 update
+// forms only the other 15 entries and sets the zeros exactly; the z-shift and the
+// Rz rotation of dh_congruence preserve the zero pattern (e_z is their axis), so
+// they skip it (the x-shift and Rx rotation fill it).
+template <typename T>
+__device__ __forceinline__ void sym6_rank1_sub_rev(Sym6<T>& K, const T* u, T invD) {
+  T w[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) w[k] = u[k] * invD;
+  K.a[0] -= w[0] * u[0]; K.a[1] -= w[1] * u[1]; K.a[2] -= w[2] * u[2];
+  K.a[3] -= w[0] * u[1]; K.a[4] -= w[0] * u[2]; K.a[5] -= w[1] * u[2];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    K.b[3 * i] -= w[i] * u[3];
+    K.b[3 * i + 1] -= w[i] * u[4];
+    K.b[3 * i + 2] = 0;
+  }
+  K.c[0] -= w[3] * u[3]; K.c[1] -= w[4] * u[4]; K.c[3] -= w[3] * u[4];
+  K.c[2] = 0; K.c[4] = 0; K.c[5] = 0;
+}
+template <typename T>
+__device__ __forceinline__ void dh_congruence_rev(T ca, T sa, T a, T d, T s, T c, Sym6<T>& K) {
+  {                                                // shift by d e_z (B col 2, C row 2 stay 0)
+    const T* A = K.a;
+    T* Bm = K.b;
+    T* C = K.c;
+    const T dd = d * d, d2 = d + d;
+    const T b00 = Bm[0], b01 = Bm[1], b10 = Bm[3], b11 = Bm[4];
+    C[0] = fma(-d2, b10, fma(dd, A[1], C[0]));
+    C[1] = fma(d2, b01, fma(dd, A[0], C[1]));
+    C[3] = fma(-d, b11, fma(d, b00, fma(-dd, A[3], C[3])));
+    Bm[0] = fma(-d, A[3], b00); Bm[1] = fma(d, A[0], b01);
+    Bm[3] = fma(-d, A[1], b10); Bm[4] = fma(d, A[3], b11);
+    Bm[6] = fma(-d, A[5], Bm[6]); Bm[7] = fma(d, A[4], Bm[7]);
+  }
+  sym_rot_plane(K.a, 0, 1, 2, c, s);               // Rz(theta)
+  {
+    T* b = K.b;                                    // B <- Rz B Rz^T, B(:, 2) = 0 stays 0
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const T bi = b[q], bj = b[3 + q];
+      b[q] = fma(c, bi, -(s * bj));
+      b[3 + q] = fma(s, bi, c * bj);
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const T bi = b[3 * r], bj = b[3 * r + 1];
+      b[3 * r] = fma(c, bi, -(s * bj));
+      b[3 * r + 1] = fma(s, bi, c * bj);
+    }
+    T* C = K.c;                                    // C <- Rz C Rz^T on the xy block only
+    const T cc = c * c, ss = s * s, cs = c * s;
+    const T cxx = C[0], cyy = C[1], cxy = C[3];
+    C[0] = fma(cc, cxx, fma(-2 * cs, cxy, ss * cyy));
+    C[1] = fma(ss, cxx, fma(2 * cs, cxy, cc * cyy));
+    C[3] = fma(cs, cxx - cyy, (cc - ss) * cxy);
+  }
+  {                                                // shift by a e_x (sym6_shift_x with B(:, 2) = 0)
+    const T* A = K.a;
+    T* Bm = K.b;
+    T* C = K.c;
+    const T aa = a * a, a2 = a + a;
+    const T b10 = Bm[3], b11 = Bm[4], b20 = Bm[6], b21 = Bm[7];
+    C[1] = fma(-a2, b21, fma(aa, A[2], C[1]));
+    C[2] = aa * A[1];
+    C[5] = fma(a, b11, -(aa * A[5]));
+    C[3] = fma(-a, b20, C[3]);
+    C[4] = a * b10;
+    Bm[1] = fma(-a, A[4], Bm[1]); Bm[2] = a * A[3];
+    Bm[4] = fma(-a, A[5], b11);   Bm[5] = a * A[1];
+    Bm[7] = fma(-a, A[2], b21);   Bm[8] = a * A[5];
+  }
+  sym_rot_plane(K.a, 1, 2, 0, ca, sa);             // Rx(alpha)
+  gen_rot_plane(K.b, 1, 2, ca, sa);
+  sym_rot_plane(K.c, 1, 2, 0, ca, sa);
+}
+
 // K += J for the link inertia J = [[m I, -[h]], [[h], I]]: only its 15 structural
 // non-zeros are added.
 template <typename T, typename CT>
@@ -245,7 +323,7 @@ __device__ __forceinline__ void sym6_add_inertia(const CT& C, Sym6<T>& K) {
 
 // y = y0 + K x for x with x[2] = x[5] = 0 (the ABA's c_i = ad_V(S qd), S = e_z or
 // e_5), y0 seeding the chains.
-template <typename T>
+template <typename T, bool R5Z = false>   // R5Z: row / column 5 of K are zero (sym6_rank1_sub_rev)
 __device__ __forceinline__ void sym6_mv_xy(const Sym6<T>& K, const T* x, const T* y0, T* y) {
   const T* A = K.a;
   const T* Bm = K.b;
@@ -256,7 +334,7 @@ __device__ __forceinline__ void sym6_mv_xy(const Sym6<T>& K, const T* x, const T
   y[2] = fma(A[4], x0, fma(A[5], x1, fma(Bm[6], x3, fma(Bm[7], x4, y0[2]))));
   y[3] = fma(Bm[0], x0, fma(Bm[3], x1, fma(C[0], x3, fma(C[3], x4, y0[3]))));
   y[4] = fma(Bm[1], x0, fma(Bm[4], x1, fma(C[3], x3, fma(C[1], x4, y0[4]))));
-  y[5] = fma(Bm[2], x0, fma(Bm[5], x1, fma(C[4], x3, fma(C[5], x4, y0[5]))));
+  y[5] = R5Z ? y0[5] : fma(Bm[2], x0, fma(Bm[5], x1, fma(C[4], x3, fma(C[5], x4, y0[5]))));
 }
 
 template <typename T>
