@@ -179,6 +179,36 @@ def test_link_counts_random_chains(rd, n):
         check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strat)
 
 
+def _wide_inertia_chain(n, seed, prismatic_fraction=0.0):
+    """random_chain with link inertias spread over many decades: mass log-uniform in
+    [1e-3, 1e3] kg, CoM up to 2 m off the joint frame, principal inertias
+    log-uniform in [1e-5, 10] kg m^2 -- stresses the kernels' inertia forms (the
+    thread / REVERSE kernels evaluate Fhat at the centre of mass, c = h / m,
+    I_c = I - m (|c|^2 1 - c c^T); ABA keeps (m, h, I) and the structural zeros)."""
+    r = synth.random_chain(n, seed, prismatic_fraction)
+    rng = np.random.default_rng(seed)
+    for i in range(n):
+        m = 10.0 ** rng.uniform(-3, 3)
+        com = rng.uniform(-2.0, 2.0, 3)
+        Rc = synth.random_rotation(rng)
+        lam = 10.0 ** rng.uniform(-5, 1, 3)
+        r["J"][i] = synth.spatial_inertia(m, com, Rc @ np.diag(lam) @ Rc.T)
+    return r
+
+
+@pytest.mark.parametrize("n", [7, 30, 100])
+def test_wide_inertia_ranges(rd, n):
+    r = _wide_inertia_chain(n, 4000 + n)
+    q, qd, qdd = synth.states(13, n, 0, 3000)
+    strats = ("auto", "thread", "reverse", "generic") + (("warp_scan",) if n <= 32 else ("block_scan",))
+    for strat in strats:
+        check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strat)
+    rp = _wide_inertia_chain(n, 4100 + n, prismatic_fraction=0.3)
+    for strat in ("thread", "reverse"):
+        check_id(rd, rp, synth.GRAVITY_Z, q, qd, qdd, strategy=strat)
+    check_fd(rd, r, synth.GRAVITY_Z, 1000, 14)               # ABA backward error <= 1e-10
+
+
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 def test_prismatic_and_screw_joints_generic(rd, dtype):
     r = synth.random_chain(12, 77, prismatic_fraction=0.5)
