@@ -177,7 +177,8 @@ template <> struct StepCfg<float, 16> {
 
 template <typename T, int PD>
 struct FwdState {
-  T V[6], Vd[6];
+  T V[6], Vd[6];                        // fp64
+  float2 VV[6];                         // fp32: (V_k, Vdot_k) packed for FFMA2 (f32x2)
   static constexpr int kPD = PD;
   T a_q[kPD], a_qd[kPD], a_qa[kPD];    // inputs of the next kPD links in stream order ([0] = current)
   const T *pq, *pqd, *pqa;              // this tile's column
@@ -185,7 +186,8 @@ struct FwdState {
 };
 template <typename T>
 struct BwdState {
-  T F[6];
+  T F[6];                       // fp64
+  float2 FF[3];                 // fp32: (f_k, m_k) packed for FFMA2
   T ca, sa, a, d, s, c;         // DH constants and stashed (sin, cos) of the child link i+1
   int64_t b;
   bool valid;
@@ -195,6 +197,114 @@ struct BwdState {
 #endif
 };
 
+// fp32 runs the per-link algebra on packed pairs (FFMA2 / FMUL2, sm_100a f32x2):
+// the forward Ad, the bias-wrench pieces and the sin/cos polynomials act on
+// (V, Vdot) component pairs, the backward Ad^T on (f, m) pairs.  Same FP32 pipe
+// rate as FFMA (measured, tools/ffma2_peak.cu) at half the issue slots; the fp32
+// kernel is issue-bound.
+template <typename T> constexpr bool kPacked = std::is_same<T, float>::value;
+template <typename T, int PD>
+__device__ __forceinline__ void fwd_unpack(FwdState<T, PD>& f) {
+  if constexpr (kPacked<T>) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) { f.V[k] = f.VV[k].x; f.Vd[k] = f.VV[k].y; }
+  }
+}
+template <typename T, int PD>
+__device__ __forceinline__ void fwd_pack(FwdState<T, PD>& f) {
+  if constexpr (kPacked<T>) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) f.VV[k] = make_float2(f.V[k], f.Vd[k]);
+  }
+}
+template <typename T>
+__device__ __forceinline__ void bwd_pack(BwdState<T>& g) {
+  if constexpr (kPacked<T>) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g.FF[k] = make_float2(g.F[k], g.F[k + 3]);
+  }
+}
+__device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+
+// (sin, cos) of q (fp32, as rd_sincos) with the two polynomials evaluated as one pair
+__device__ __forceinline__ void sincos_f32x2(float x, float* sp, float* cp) {
+  const float k = rintf(x * 0.636619772f);
+  const int quad = (int)k;
+  float r = fmaf(-k, 1.57079637f, x);
+  r = fmaf(-k, -4.37113883e-08f, r);
+  r = fmaf(-k, -1.71512489e-15f, r);
+  const float z = r * r;
+  const float2 Z = f2(z);
+  float2 P = fma2(Z, make_float2(-1.9515295891e-4f, 2.443315711809948e-5f),
+                  make_float2(8.3321608736e-3f, -1.388731625493765e-3f));
+  P = fma2(Z, P, make_float2(-1.6666654611e-1f, 4.166664568298827e-2f));
+  const float2 SC = fma2(mul2(Z, make_float2(r, z)), P, make_float2(r, fmaf(-0.5f, z, 1.0f)));
+  const float sn = SC.x, cs = SC.y;
+  const float a = (quad & 1) ? cs : sn;
+  const float b = (quad & 1) ? sn : cs;
+  *sp = (quad & 2) ? -a : a;
+  *cp = ((quad + 1) & 2) ? -b : b;
+}
+
+// Ad_{f^-1} of dh_ad_finv (rd_math.cuh) on the pair (V, Vdot), lane-wise
+__device__ __forceinline__ void dh_ad_finv_x2(float ca, float sa, float a, float d, float s, float c,
+                                              const float2* in, float2* out) {
+  const float2 CA = f2(ca), SA = f2(sa), NSA = f2(-sa), C = f2(c), S = f2(s), NS = f2(-s);
+  float2 v1 = fma2(CA, in[1], mul2(SA, in[2])), v2 = fma2(CA, in[2], mul2(NSA, in[1]));
+  const float2 w1 = fma2(CA, in[4], mul2(SA, in[5])), w2 = fma2(CA, in[5], mul2(NSA, in[4]));
+  v1 = fma2(f2(a), w2, v1);
+  v2 = fma2(f2(-a), w1, v2);
+  const float2 W0 = fma2(C, in[3], mul2(S, w1)), W1 = fma2(C, w1, mul2(NS, in[3]));
+  const float2 V0 = fma2(C, in[0], mul2(S, v1)), V1 = fma2(C, v1, mul2(NS, in[0]));
+  out[0] = fma2(f2(d), W1, V0);
+  out[1] = fma2(f2(-d), W0, V1);
+  out[2] = v2; out[3] = W0; out[4] = W1; out[5] = w2;
+}
+
+// Fhat at the centre of mass (bias_force_com, rd_math.cuh) from the pairs (V, Vdot);
+// out = (f0, n0, f1, n1, f2, n2), the (f, m) pair order of the backward sweep
+template <typename CT>
+__device__ __forceinline__ void bias_force_com_x2(const CT& C, const float2* VV, float* out) {
+  const float c0 = C.c[0], c1 = C.c[1], c2 = C.c[2];
+  // (v_c, a_c) = (v, vd) + (w, wd) x c
+  const float2 P0 = fma2(VV[4], f2(c2), fma2(VV[5], f2(-c1), VV[0]));
+  const float2 P1 = fma2(VV[5], f2(c0), fma2(VV[3], f2(-c2), VV[1]));
+  const float2 P2 = fma2(VV[3], f2(c1), fma2(VV[4], f2(-c0), VV[2]));
+  const float w0 = VV[3].x, w1 = VV[4].x, w2 = VV[5].x;
+  const float f0 = C.m * fmaf(w1, P2.x, fmaf(-w2, P1.x, P0.y));
+  const float f1 = C.m * fmaf(w2, P0.x, fmaf(-w0, P2.x, P1.y));
+  const float f2v = C.m * fmaf(w0, P1.x, fmaf(-w1, P0.x, P2.y));
+  // (I_c w, I_c wd)
+  const float Ixx = C.Ic[0], Iyy = C.Ic[1], Izz = C.Ic[2], Ixy = C.Ic[3], Ixz = C.Ic[4], Iyz = C.Ic[5];
+  const float2 L0 = fma2(f2(Ixx), VV[3], fma2(f2(Ixy), VV[4], mul2(f2(Ixz), VV[5])));
+  const float2 L1 = fma2(f2(Ixy), VV[3], fma2(f2(Iyy), VV[4], mul2(f2(Iyz), VV[5])));
+  const float2 L2 = fma2(f2(Ixz), VV[3], fma2(f2(Iyz), VV[4], mul2(f2(Izz), VV[5])));
+  out[0] = f0; out[2] = f1; out[4] = f2v;
+  out[1] = fmaf(c1, f2v, fmaf(-c2, f1, fmaf(w1, L2.x, fmaf(-w2, L1.x, L0.y))));
+  out[3] = fmaf(c2, f0, fmaf(-c0, f2v, fmaf(w2, L0.x, fmaf(-w0, L2.x, L1.y))));
+  out[5] = fmaf(c0, f1, fmaf(-c1, f0, fmaf(w0, L1.x, fmaf(-w1, L0.x, L2.y))));
+}
+
+// F = Fh + Ad^T_{f^-1} Fn of dh_bwd (rd_math.cuh) on the pairs (f_k, m_k); Fh in the
+// pair order (f0, n0, f1, n1, f2, n2)
+__device__ __forceinline__ void dh_bwd_x2(float ca, float sa, float a, float d, float s, float c,
+                                          const float2* Fn, const float* Fh, float2* F) {
+  // Tz(d): m += d e_z x f = d (-f1, f0, 0)   (m lanes)
+  const float2 p0 = make_float2(Fn[0].x, fmaf(-d, Fn[1].x, Fn[0].y));
+  const float2 p1 = make_float2(Fn[1].x, fmaf(d, Fn[0].x, Fn[1].y));
+  // Rz; the x rows are final
+  F[0] = fma2(f2(c), p0, fma2(f2(-s), p1, make_float2(Fh[0], Fh[1])));
+  float2 g1 = fma2(f2(s), p0, mul2(f2(c), p1));
+  // Tx(a): m += a e_x x f = a (0, -f2, f1)
+  g1.y = fmaf(-a, Fn[2].x, g1.y);
+  const float2 g2 = make_float2(Fn[2].x, fmaf(a, g1.x, Fn[2].y));
+  // Rx, + Fh
+  F[1] = fma2(f2(ca), g1, fma2(f2(-sa), g2, make_float2(Fh[2], Fh[3])));
+  F[2] = fma2(f2(sa), g1, fma2(f2(ca), g2, make_float2(Fh[4], Fh[5])));
+}
+
 // Inputs are consumed as ONE stream over (tile, link): the loads issued at link
 // k fetch link k+2 of this tile, or link k+2-n of the NEXT tile, so the first
 // links of a tile are already in registers when its forward sweep starts.
@@ -202,7 +312,10 @@ template <typename T, int PD>
 __device__ __forceinline__ void fwd_init(FwdState<T, PD>& f, const ThreadParams<T>& P, int64_t B, int64_t bl,
                                          int64_t bl_next, const T* q, const T* qd, const T* qdd, bool first) {
 #pragma unroll
-  for (int k = 0; k < 6; ++k) { f.V[k] = P.bnd.V0[k]; f.Vd[k] = P.bnd.Vd0[k]; }
+  for (int k = 0; k < 6; ++k) {
+    if constexpr (kPacked<T>) f.VV[k] = make_float2(P.bnd.V0[k], P.bnd.Vd0[k]);
+    else { f.V[k] = P.bnd.V0[k]; f.Vd[k] = P.bnd.Vd0[k]; }
+  }
   f.pq = q + bl; f.pqd = qd + bl; f.pqa = qdd + bl;
   f.xq = q + bl_next; f.xqd = qd + bl_next; f.xqa = qdd + bl_next;
   if (first) {
@@ -230,6 +343,10 @@ __device__ __forceinline__ void bwd_init(BwdState<T>& g, const ThreadParams<T>& 
 #endif
 #pragma unroll
   for (int k = 0; k < 6; ++k) g.F[k] = P.bnd.Ftip[k];
+  if constexpr (kPacked<T>) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g.FF[k] = make_float2(P.bnd.Ftip[k], P.bnd.Ftip[k + 3]);
+  }
   g.ca = 1; g.sa = 0; g.a = g.d = 0; g.s = 0; g.c = 1;   // f_{n,n+1} = I (A5)
 }
 // forward link k: V_k, Vdot_k, Fhat_k -> st[8]
@@ -252,16 +369,35 @@ __device__ __forceinline__ void fwd_link(FwdState<T, PD>& f, const ThreadParams<
   const bool prism = PR && ((P.prism >> k) & 1u);
   const T qang = prism ? T(0) : cq;               // revolute: theta = th0 + q; prismatic: th0
   T s, c;
-  if (sizeof(T) == 8) {
+  if constexpr (sizeof(T) == 8) {
     rd_sincos(qang + C.th0, &s, &c);          // fp64: rounding of q + th0 is ~ulp(q)
   } else {
     T s0, c0;                                     // fp32: sin/cos(q) then add th0 exactly
-    rd_sincos(qang, &s0, &c0);
+    sincos_f32x2(qang, &s0, &c0);
     s = fma(s0, C.cth0, c0 * C.sth0);
     c = fma(c0, C.cth0, -(s0 * C.sth0));
   }
   // Eq. (1): V = Ad_{f^-1} V + S qd, Vd = Ad_{f^-1} Vd + S qdd + ad_V(S qd),
   // S = (0, e_z) (revolute) or (e_z, 0) (prismatic, d = d0 + q)
+  if constexpr (kPacked<T>) {
+    float2 VVn[6];
+    const float dl = PR && prism ? C.d + cq : C.d;
+    dh_ad_finv_x2(C.ca, C.sa, C.a, dl, s, c, f.VV, VVn);
+    const float sr = prism ? 0.f : cqd, sp = prism ? cqd : 0.f;
+    const float ar = prism ? 0.f : cqa, ap = prism ? cqa : 0.f;
+    VVn[5] = __fadd2_rn(VVn[5], make_float2(sr, ar));
+    if (PR) VVn[2] = __fadd2_rn(VVn[2], make_float2(sp, ap));
+    // ad_V (sp e_z, sr e_z) into the Vdot lanes
+    VVn[0].y = fmaf(sr, VVn[1].x, PR ? fmaf(sp, VVn[4].x, VVn[0].y) : VVn[0].y);
+    VVn[1].y = fmaf(-sr, VVn[0].x, PR ? fmaf(-sp, VVn[3].x, VVn[1].y) : VVn[1].y);
+    VVn[3].y = fmaf(sr, VVn[4].x, VVn[3].y);
+    VVn[4].y = fmaf(-sr, VVn[3].x, VVn[4].y);
+    st[0] = (PR && prism) ? cq : s;
+    st[1] = c;
+    bias_force_com_x2(C, VVn, st + 2);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) f.VV[j] = VVn[j];
+  } else {
   T Vn[6], Vdn[6];
   if (PR) {
     const T dq = prism ? cq : T(0);
@@ -295,6 +431,7 @@ __device__ __forceinline__ void fwd_link(FwdState<T, PD>& f, const ThreadParams<
   bias_force_com(C, Vn, Vdn, st + 2);
 #pragma unroll
   for (int j = 0; j < 6; ++j) { f.V[j] = Vn[j]; f.Vd[j] = Vdn[j]; }
+  }
 #pragma unroll
   for (int j = 0; j + 1 < kPD; ++j) { f.a_q[j] = f.a_q[j + 1]; f.a_qd[j] = f.a_qd[j + 1]; f.a_qa[j] = f.a_qa[j + 1]; }
   f.a_q[kPD - 1] = f_q; f.a_qd[kPD - 1] = f_qd; f.a_qa[kPD - 1] = f_qa;
@@ -309,12 +446,21 @@ __device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& 
   // it right after the chain stalled the warp on the fixed-latency dependency)
   if (g.valid && g.ip >= 0) tau[(int64_t)g.ip * B + g.b] = g.tp;
 #endif
-  dh_bwd(g.ca, g.sa, g.a, g.d, g.s, g.c, g.F, cur + 2, Fo);
-#pragma unroll
-  for (int j = 0; j < 6; ++j) g.F[j] = Fo[j];
   const LinkDHc<T>& C = P.L[i];
   const bool prism = PR && ((P.prism >> i) & 1u);
-  const T ti = prism ? g.F[2] : g.F[5];            // tau_i = S_i^T F_i
+  T ti;                                            // tau_i = S_i^T F_i
+  if constexpr (kPacked<T>) {
+    float2 F2[3];
+    dh_bwd_x2(g.ca, g.sa, g.a, g.d, g.s, g.c, g.FF, cur + 2, F2);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) g.FF[j] = F2[j];
+    ti = prism ? g.FF[2].x : g.FF[2].y;
+  } else {
+    dh_bwd(g.ca, g.sa, g.a, g.d, g.s, g.c, g.F, cur + 2, Fo);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) g.F[j] = Fo[j];
+    ti = prism ? g.F[2] : g.F[5];
+  }
 #if RD_TAU_DEFER
   g.tp = ti;
   g.ip = i;
@@ -427,7 +573,7 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
       const int bpar = (int)((it - 1) & 1);
       bwd_init(g, P);
       if constexpr (SB) {                            // per-state F_{n+1} of tile it-1 (NEXT-4)
-        if (sb.Ft) sb_vec(sb.Ft, sb.At, B, min(g.b, B - 1), g.F);
+        if (sb.Ft) { sb_vec(sb.Ft, sb.At, B, min(g.b, B - 1), g.F); bwd_pack(g); }
       }
       for (int i = n - 1; i >= 0; --i) {
         T cur[8];
@@ -440,8 +586,12 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
     const int64_t bn = b + (int64_t)gridDim.x * NT;
     fwd_init(f, P, B, fvalid ? b : (B - 1), bn < B ? bn : (B - 1), q, qd, qdd, it == 0 || P.n < Cfg::kPD);
     if constexpr (SB) {                              // per-state V_0, Vdot_0 (NEXT-4)
-      if (sb.V0) sb_vec(sb.V0, sb.A0, B, fvalid ? b : (B - 1), f.V);
-      if (sb.Vd0) sb_vec(sb.Vd0, sb.A0, B, fvalid ? b : (B - 1), f.Vd);
+      if (sb.V0 || sb.Vd0) {
+        fwd_unpack(f);
+        if (sb.V0) sb_vec(sb.V0, sb.A0, B, fvalid ? b : (B - 1), f.V);
+        if (sb.Vd0) sb_vec(sb.Vd0, sb.A0, B, fvalid ? b : (B - 1), f.Vd);
+        fwd_pack(f);
+      }
     }
     if (it == 0) {
       // prologue: forward of the first tile alone (parity 0: slot = link)
@@ -455,7 +605,7 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
       // at step k both use slot s_k = bpar ? k : n-1-k.
       bwd_init(g, P);
       if constexpr (SB) {                            // per-state F_{n+1} of tile it-1 (NEXT-4)
-        if (sb.Ft) sb_vec(sb.Ft, sb.At, B, min(g.b, B - 1), g.F);
+        if (sb.Ft) { sb_vec(sb.Ft, sb.At, B, min(g.b, B - 1), g.F); bwd_pack(g); }
       }
       const int bpar = (int)((it - 1) & 1);
       auto smem_step = [&](int k) {
