@@ -316,7 +316,8 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
       const T ub = (ct - ((PR && pz) ? ph[2] : ph[5])) * invD;
       T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) w[k * slots] = U[k] * invD;
+      for (int k = 0; k < 6; ++k)
+        if (PR || k != 5) w[k * slots] = U[k] * invD;   // revolute: Ubar_5 = U_5 / D = 1, not stored
       w[6 * slots] = ub;
       if (i > 0) {
         if constexpr (PR) sym6_rank1_sub(K, U, invD);     // Jhat^a
@@ -370,7 +371,8 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
 #pragma unroll
       for (int j = 0; j < PD; ++j)
 #pragma unroll
-        for (int k = 0; k < 7; ++k) cU[j][k] = ws[((int64_t)min(j, n - 1) * kAbaPerLink + k) * slots + slot];
+        for (int k = 0; k < 7; ++k)
+          cU[j][k] = (PR || k != 5) ? ws[((int64_t)min(j, n - 1) * kAbaPerLink + k) * slots + slot] : T(1);
 #endif
 #pragma unroll (kS3U)
       for (int i = 0; i < n; ++i) {
@@ -394,7 +396,7 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
         {
           const T* wn = ws + (int64_t)min(i + PD, n - 1) * kAbaPerLink * slots + slot;
 #pragma unroll
-          for (int k = 0; k < 7; ++k) cU[PD - 1][k] = wn[k * slots];
+          for (int k = 0; k < 7; ++k) cU[PD - 1][k] = (PR || k != 5) ? wn[k * slots] : T(1);
         }
 #else
         const T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
