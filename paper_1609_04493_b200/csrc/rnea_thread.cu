@@ -162,9 +162,12 @@ template <typename T, int W> struct StepCfg {
   static constexpr int kPD = RD_PD64W16, kUnroll = RD_U64W16;
   static constexpr bool kFwdFirst = false;
 };
+#ifndef RD_FWDFIRST64
+#define RD_FWDFIRST64 0
+#endif
 template <> struct StepCfg<double, 8> {
   static constexpr int kPD = RD_PD64, kUnroll = RD_U64;
-  static constexpr bool kFwdFirst = false;
+  static constexpr bool kFwdFirst = RD_FWDFIRST64;
 };
 template <> struct StepCfg<float, 8> {
   static constexpr int kPD = RD_PD32, kUnroll = RD_U32;
