@@ -33,6 +33,9 @@ namespace rd {
 #endif
 // Input prefetch distances / unroll factors of the DH kernel's sweeps 1 and 3
 // (short iterations; see rnea_thread.cu StepCfg for why unroll ~ distance).
+#ifndef RD_ABA_MB
+#define RD_ABA_MB 3            // DH kernel: min CTAs of kAbaThreads per SM (register cap)
+#endif
 #ifndef RD_ABA_S1PD
 #define RD_ABA_S1PD 4
 #endif
@@ -453,11 +456,11 @@ static cudaError_t launch_aba_dh_pr(int n, const LinkDH<T>* L_dev, const Boundar
   const int64_t grid = (ws_slots + kAbaThreads - 1) / kAbaThreads;
   const size_t smem = (size_t)n * sizeof(LinkDH<T>) + (PR ? (size_t)n : 0);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(aba_dh_kernel<T, 3, PR, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(aba_dh_kernel<T, RD_ABA_MB, PR, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  aba_dh_kernel<T, 3, PR, SB><<<(unsigned)grid, kAbaThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws,
+  aba_dh_kernel<T, RD_ABA_MB, PR, SB><<<(unsigned)grid, kAbaThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws,
                                                                           ws_slots, status, prism, sb);
   return cudaGetLastError();
 }
