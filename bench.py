@@ -120,9 +120,15 @@ def cpu_baseline(robot, g, cfg, n, seconds=10.0):
         t_total += time.perf_counter() - t0
         done += chunk
         b0 += chunk
-    return {"value": done / t_total, "unit": UNIT, "cores": cores, "kind": "oracle",
+    # single-core figure: one thread on the first chunk, ~1-2 s
+    q, qd, qdd = synth.states(cfg["seed"], n, 0, chunk, cfg["ranges"])
+    t0 = time.perf_counter()
+    oracle.rnea_batch(robot, g, q, qd, qdd, nthreads=1)
+    one = chunk / (time.perf_counter() - t0)
+    return {"value": done / t_total, "unit": UNIT, "cores": cores, "kind": "oracle", "single_core_value": one,
             "sample": f"first {done} states of the {cfg['name']} workload (n={n}), oracle::rnea "
-                      f"(C++ -O2, dense 6x6 Eq. 1-2) on {cores} host threads, {t_total:.1f} s"}
+                      f"(C++ -O2, dense 6x6 Eq. 1-2) on {cores} host threads, {t_total:.1f} s; "
+                      f"single_core_value: {chunk} states on 1 thread"}
 
 
 def cpu_baseline_fd(robot, g, cfg, n, seconds=10.0):
@@ -139,9 +145,15 @@ def cpu_baseline_fd(robot, g, cfg, n, seconds=10.0):
         t_total += time.perf_counter() - t0
         done += chunk
         b0 += chunk
-    return {"value": done / t_total, "unit": UNIT, "cores": cores, "kind": "oracle",
+    q, qd, qdd = synth.states(cfg["seed"], n, 0, chunk, cfg["ranges"])
+    tau = oracle.rnea_batch(robot, g, q, qd, qdd, nthreads=cores)
+    t0 = time.perf_counter()
+    oracle.fd_batch(robot, g, q, qd, tau, nthreads=1)
+    one = chunk / (time.perf_counter() - t0)
+    return {"value": done / t_total, "unit": UNIT, "cores": cores, "kind": "oracle", "single_core_value": one,
             "sample": f"first {done} states of the {cfg['name']} FD workload (n={n}), oracle::fd_aba "
-                      f"(C++ -O2, Eq. 7-8) on {cores} host threads, {t_total:.1f} s"}
+                      f"(C++ -O2, Eq. 7-8) on {cores} host threads, {t_total:.1f} s; "
+                      f"single_core_value: {chunk} states on 1 thread"}
 
 
 def load_traffic(cfg_name: str, dtype: str):
