@@ -231,6 +231,11 @@ __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
+// Cephes sinf / cosf coefficient pairs (S3, C3), (S2, C2), (S1, C1) as constant-bank
+// operands of FFMA2 (immediates would be rebuilt into register pairs every link)
+static __constant__ float2 kSinCos32x2[3] = {{-1.9515295891e-4f, 2.443315711809948e-5f},
+                                             {8.3321608736e-3f, -1.388731625493765e-3f},
+                                             {-1.6666654611e-1f, 4.166664568298827e-2f}};
 // (sin, cos) of q (fp32, as rd_sincos) with the two polynomials evaluated as one pair
 __device__ __forceinline__ void sincos_f32x2(float x, float* sp, float* cp) {
   const float k = rintf(x * 0.636619772f);
@@ -240,9 +245,8 @@ __device__ __forceinline__ void sincos_f32x2(float x, float* sp, float* cp) {
   r = fmaf(-k, -1.71512489e-15f, r);
   const float z = r * r;
   const float2 Z = f2(z);
-  float2 P = fma2(Z, make_float2(-1.9515295891e-4f, 2.443315711809948e-5f),
-                  make_float2(8.3321608736e-3f, -1.388731625493765e-3f));
-  P = fma2(Z, P, make_float2(-1.6666654611e-1f, 4.166664568298827e-2f));
+  float2 P = fma2(Z, kSinCos32x2[0], kSinCos32x2[1]);
+  P = fma2(Z, P, kSinCos32x2[2]);
   const float2 SC = fma2(mul2(Z, make_float2(r, z)), P, make_float2(r, fmaf(-0.5f, z, 1.0f)));
   const float sn = SC.x, cs = SC.y;
   const float a = (quad & 1) ? cs : sn;
@@ -290,22 +294,24 @@ __device__ __forceinline__ void bias_force_com_x2(const CT& C, const float2* VV,
   out[5] = fmaf(c0, f1, fmaf(-c1, f0, fmaf(w0, L1.x, fmaf(-w1, L0.x, L2.y))));
 }
 
-// F = Fh + Ad^T_{f^-1} Fn of dh_bwd (rd_math.cuh) on the pairs (f_k, m_k); Fh in the
-// pair order (f0, n0, f1, n1, f2, n2)
+// F <- Fh + Ad^T_{f^-1} F of dh_bwd (rd_math.cuh) on the pairs FF[k] = (f_k, m_k),
+// updated in place (lane updates, so no pair is re-assembled); Fh in the pair
+// order (f0, n0, f1, n1, f2, n2)
 __device__ __forceinline__ void dh_bwd_x2(float ca, float sa, float a, float d, float s, float c,
-                                          const float2* Fn, const float* Fh, float2* F) {
+                                          float2* FF, const float* Fh) {
   // Tz(d): m += d e_z x f = d (-f1, f0, 0)   (m lanes)
-  const float2 p0 = make_float2(Fn[0].x, fmaf(-d, Fn[1].x, Fn[0].y));
-  const float2 p1 = make_float2(Fn[1].x, fmaf(d, Fn[0].x, Fn[1].y));
+  FF[0].y = fmaf(-d, FF[1].x, FF[0].y);
+  FF[1].y = fmaf(d, FF[0].x, FF[1].y);
   // Rz; the x rows are final
-  F[0] = fma2(f2(c), p0, fma2(f2(-s), p1, make_float2(Fh[0], Fh[1])));
-  float2 g1 = fma2(f2(s), p0, mul2(f2(c), p1));
+  const float2 F0 = fma2(f2(c), FF[0], fma2(f2(-s), FF[1], make_float2(Fh[0], Fh[1])));
+  float2 g1 = fma2(f2(s), FF[0], mul2(f2(c), FF[1]));
   // Tx(a): m += a e_x x f = a (0, -f2, f1)
-  g1.y = fmaf(-a, Fn[2].x, g1.y);
-  const float2 g2 = make_float2(Fn[2].x, fmaf(a, g1.x, Fn[2].y));
+  g1.y = fmaf(-a, FF[2].x, g1.y);
+  FF[2].y = fmaf(a, g1.x, FF[2].y);
   // Rx, + Fh
-  F[1] = fma2(f2(ca), g1, fma2(f2(-sa), g2, make_float2(Fh[2], Fh[3])));
-  F[2] = fma2(f2(sa), g1, fma2(f2(ca), g2, make_float2(Fh[4], Fh[5])));
+  const float2 F1 = fma2(f2(ca), g1, fma2(f2(-sa), FF[2], make_float2(Fh[2], Fh[3])));
+  const float2 F2 = fma2(f2(sa), g1, fma2(f2(ca), FF[2], make_float2(Fh[4], Fh[5])));
+  FF[0] = F0; FF[1] = F1; FF[2] = F2;
 }
 
 // Inputs are consumed as ONE stream over (tile, link): the loads issued at link
@@ -388,8 +394,8 @@ __device__ __forceinline__ void fwd_link(FwdState<T, PD>& f, const ThreadParams<
     dh_ad_finv_x2(C.ca, C.sa, C.a, dl, s, c, f.VV, VVn);
     const float sr = prism ? 0.f : cqd, sp = prism ? cqd : 0.f;
     const float ar = prism ? 0.f : cqa, ap = prism ? cqa : 0.f;
-    VVn[5] = __fadd2_rn(VVn[5], make_float2(sr, ar));
-    if (PR) VVn[2] = __fadd2_rn(VVn[2], make_float2(sp, ap));
+    VVn[5].x += sr; VVn[5].y += ar;                 // lane adds: no pair to assemble
+    if (PR) { VVn[2].x += sp; VVn[2].y += ap; }
     // ad_V (sp e_z, sr e_z) into the Vdot lanes
     VVn[0].y = fmaf(sr, VVn[1].x, PR ? fmaf(sp, VVn[4].x, VVn[0].y) : VVn[0].y);
     VVn[1].y = fmaf(-sr, VVn[0].x, PR ? fmaf(-sp, VVn[3].x, VVn[1].y) : VVn[1].y);
@@ -453,10 +459,7 @@ __device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& 
   const bool prism = PR && ((P.prism >> i) & 1u);
   T ti;                                            // tau_i = S_i^T F_i
   if constexpr (kPacked<T>) {
-    float2 F2[3];
-    dh_bwd_x2(g.ca, g.sa, g.a, g.d, g.s, g.c, g.FF, cur + 2, F2);
-#pragma unroll
-    for (int j = 0; j < 3; ++j) g.FF[j] = F2[j];
+    dh_bwd_x2(g.ca, g.sa, g.a, g.d, g.s, g.c, g.FF, cur + 2);
     ti = prism ? g.FF[2].x : g.FF[2].y;
   } else {
     dh_bwd(g.ca, g.sa, g.a, g.d, g.s, g.c, g.F, cur + 2, Fo);
