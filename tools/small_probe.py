@@ -53,22 +53,27 @@ def graph(fn, k=20):
     return float(np.median(ts)) * 1e3 / k
 
 
-cfgs = sys.argv[1:] or ["C2"]
-print("config,dtype,B,strategy,single_us,b2b_us,graph_us")
-for name in cfgs:
-    cfg = synth.CONFIGS[name]
-    n = cfg["n"]
-    model = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
-    for dt in (torch.float64, torch.float32):
-        for B in (1, 1000, 10000, 100000):
-            q, qd, qdd = (torch.from_numpy(x).to("cuda", dt) for x in synth.states(cfg["seed"], n, 0, B, cfg["ranges"]))
-            out = torch.empty_like(q)
-            for strat in ("auto", "thread", "reverse", "warp_scan"):
-                model.set_strategy(strat)
-                fn = lambda: rd.inverse_dynamics(model, q, qd, qdd, out)  # noqa: E731
-                for _ in range(5):
-                    fn()
-                torch.cuda.synchronize()
-                name_s = model.resolve_strategy(B, dt == torch.float64) if strat == "auto" else strat
-                print(f"{name},{str(dt)[6:]},{B},{strat}:{name_s},{single(fn):.1f},{b2b(fn):.1f},{graph(fn):.1f}",
-                      flush=True)
+def main():
+    cfgs = sys.argv[1:] or ["C2"]
+    print("config,dtype,B,strategy,single_us,b2b_us,graph_us")
+    for name in cfgs:
+        cfg = synth.CONFIGS[name]
+        n = cfg["n"]
+        model = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
+        for dt in (torch.float64, torch.float32):
+            for B in (1, 1000, 10000, 100000):
+                q, qd, qdd = (torch.from_numpy(x).to("cuda", dt) for x in synth.states(cfg["seed"], n, 0, B, cfg["ranges"]))
+                out = torch.empty_like(q)
+                for strat in ("auto", "thread", "reverse", "warp_scan"):
+                    model.set_strategy(strat)
+                    fn = lambda: rd.inverse_dynamics(model, q, qd, qdd, out)  # noqa: E731
+                    for _ in range(5):
+                        fn()
+                    torch.cuda.synchronize()
+                    name_s = model.resolve_strategy(B, dt == torch.float64) if strat == "auto" else strat
+                    print(f"{name},{str(dt)[6:]},{B},{strat}:{name_s},{single(fn):.1f},{b2b(fn):.1f},{graph(fn):.1f}",
+                          flush=True)
+
+
+if __name__ == "__main__":
+    main()
