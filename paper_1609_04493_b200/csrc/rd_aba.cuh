@@ -337,16 +337,6 @@ __device__ __forceinline__ void sym6_mv_xy(const Sym6<T>& K, const T* x, const T
   y[5] = R5Z ? y0[5] : fma(Bm[2], x0, fma(Bm[5], x1, fma(C[4], x3, fma(C[5], x4, y0[5]))));
 }
 
-template <typename T>
-__device__ __forceinline__ void dh_inertia(const LinkDH<T>& C, Sym6<T>& K) {
-  K.a[0] = C.m; K.a[1] = C.m; K.a[2] = C.m; K.a[3] = 0; K.a[4] = 0; K.a[5] = 0;
-  const T h0 = C.h[0], h1 = C.h[1], h2 = C.h[2];
-  K.b[0] = 0;   K.b[1] = h2;  K.b[2] = -h1;
-  K.b[3] = -h2; K.b[4] = 0;   K.b[5] = h0;
-  K.b[6] = h1;  K.b[7] = -h0; K.b[8] = 0;
-#pragma unroll
-  for (int k = 0; k < 6; ++k) K.c[k] = C.I[k];
-}
 
 template <typename T>
 __device__ __forceinline__ void dh_sincos(const LinkDH<T>& C, T q, T* s, T* c) {
