@@ -252,6 +252,9 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--gather", action="store_true", help="time a final all-gather of tau (off the hot path)")
+    ap.add_argument("--check-gather", action="store_true", help="with --gather: check the gathered tau")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: ranks may share one GPU)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=65536)
@@ -267,10 +270,18 @@ def main():
     import paper_1609_04493_b200 as rd
 
     world, rank, local = dist_env()
+    # one process per GPU; --backend gloo runs the same multi-rank path with several
+    # ranks sharing the visible GPU(s) (a test of the host logic, not a scaling run)
+    ndev = torch.cuda.device_count()
+    local = local % ndev if args.backend == "gloo" else local
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    coll_dev = "cuda" if args.backend == "nccl" else "cpu"     # where the off-path collectives run
     cfg = config_of(args)
     n = cfg["n"]
     fd = args.config == "C4"
@@ -282,11 +293,11 @@ def main():
     robot = robot_of(cfg)
     g = cfg["gravity"]
     dt = torch.float64 if args.dtype == "f64" else torch.float32
-    # inputs: a pure function of the GLOBAL state index (any shard regenerates its slice)
-    q, qd, qdd = synth.states(cfg["seed"], n, b0, b1, cfg["ranges"])
+    # inputs: a pure function of the GLOBAL state index, generated on this rank's GPU
+    # (synth/gen.cu: bit-identical to synth.states, which the CPU oracle side uses)
+    tq, tqd, tqdd = synth.states_device(cfg["seed"], n, b0, b1, cfg["ranges"], dtype=dt)
     model = rd.Model.from_robot(robot, g)
     model.set_strategy(args.strategy)
-    tq, tqd, tqdd = (torch.from_numpy(x).to("cuda", dt) for x in (q, qd, qdd))
     out = torch.empty_like(tq)
     if fd:
         tau_in = rd.inverse_dynamics(model, tq, tqd, tqdd)     # consistent torques (untimed)
@@ -303,6 +314,15 @@ def main():
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
+
+    def allreduce_max(vals):
+        """MAX over ranks of a few floats (the timing reduction, off the hot path)."""
+        if world == 1:
+            return vals
+        import torch.distributed as dist
+        tt = torch.tensor(vals, device=coll_dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return [float(x) for x in tt]
 
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -330,11 +350,7 @@ def main():
     kernel_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = t_start.elapsed_time(t_end) if flush_buf is None else sum(kernel_ms)
     avg_kernel_ms = float(np.mean(kernel_ms))
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([total_ms, avg_kernel_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms, avg_kernel_ms = float(tt[0]), float(tt[1])
+    total_ms, avg_kernel_ms = allreduce_max([total_ms, avg_kernel_ms])
     units = total * args.steps
     value = units / (total_ms / 1e3)
 
@@ -344,16 +360,18 @@ def main():
         import torch.distributed as dist
         barrier()
         g0 = time.perf_counter()
-        full = gather_rows(out, total)
+        full = gather_rows(out if coll_dev == "cuda" else out.cpu(), total)
         torch.cuda.synchronize()
+        if args.check_gather:                         # every rank holds the full tau: compare its own slice
+            assert torch.equal(full[:, b0:b1].to(out.device), out), "gathered tau differs from the shard"
         gather_ms = (time.perf_counter() - g0) * 1e3
         del full
 
     # e2e: through the public host-buffer API (pinned host arrays, H2D + kernel + D2H per step)
     e2e = None
     if args.dtype == "f64" and args.e2e_steps > 0:
-        third = tau_in.cpu().numpy() if fd else qdd                # FD: the consistent torques
-        pq, pqd, pqdd = (torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (q, qd, third))
+        third = tau_in if fd else tqdd                             # FD: the consistent torques
+        pq, pqd, pqdd = (x.cpu().pin_memory() for x in (tq, tqd, third))
         pout = torch.empty_like(pq).pin_memory()
         host_api = rd.forward_dynamics_host if fd else rd.inverse_dynamics_host
         host_api(model, pq, pqd, pqdd, pout)
@@ -361,12 +379,7 @@ def main():
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             host_api(model, pq, pqd, pqdd, pout)
-        e2e_s = time.perf_counter() - t0
-        if world > 1:
-            import torch.distributed as dist
-            tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = float(tt[0])
+        e2e_s = allreduce_max([time.perf_counter() - t0])[0]
         e2e = {"value": total * args.e2e_steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": 3 * n * total * 8, "d2h_bytes_per_step": n * total * 8,
                "api": ("rd_forward_dynamics_host_f64" if fd else "rd_inverse_dynamics_host_f64")

@@ -110,8 +110,12 @@ rd_status_t rd_model_create(int32_t n, const double* M, const double* S, const d
 
 rd_status_t rd_model_destroy(rd_model_t m);
 
-/* Number of links n. */
+/* Number of links n (-1 for a NULL model). */
 int32_t rd_model_n(rd_model_t m);
+
+/* CUDA device ordinal the model was created on (-1 for a NULL model); every
+ * device pointer passed with this model must be memory of that device. */
+int32_t rd_model_device(rd_model_t m);
 
 /* Override the inverse-dynamics strategy (RD_STRAT_AUTO restores the table). */
 rd_status_t rd_model_set_strategy(rd_model_t m, rd_strategy_t s);
@@ -133,8 +137,14 @@ rd_status_t rd_inverse_dynamics_f32(rd_model_t m, int64_t batch, const float* q,
                                     const float* qdd, float* tau, void* stream);
 
 /* Forward dynamics (Eq. 4) on DEVICE arrays [n][batch]; qdd is written.
- * Uses a per-model device workspace, so concurrent FD calls on ONE model must be
- * serialised by the caller (one model per stream otherwise). */
+ * Concurrency (ID and FD alike): a model may be used by several host threads and
+ * streams at once.  Calls that need a workspace (GENERIC ID, every FD algorithm)
+ * allocate it per call, stream-ordered, from the model's memory pool
+ * (cudaMallocFromPoolAsync before the kernels, cudaFreeAsync after them on the
+ * call's stream), so concurrent calls never share scratch memory and a call
+ * captured in a CUDA graph owns its workspace in the graph.  The model's
+ * constants are read-only after creation; rd_model_set_* must not race with
+ * calls on the same model. */
 rd_status_t rd_forward_dynamics_f64(rd_model_t m, int64_t batch, const double* q, const double* qd,
                                     const double* tau, double* qdd, void* stream);
 rd_status_t rd_forward_dynamics_f32(rd_model_t m, int64_t batch, const float* q, const float* qd,
@@ -179,7 +189,10 @@ rd_status_t rd_forward_dynamics_ex_f32(rd_model_t m, int64_t batch, const float*
 /* End-to-end inverse dynamics on HOST arrays [n][batch] (pageable or pinned):
  * the library streams the batch through device buffers in chunks, overlapping
  * host->device copies, the kernel and device->host copies on its own streams,
- * and returns after tau is complete in host memory (synchronous). */
+ * and returns after tau is complete in host memory (synchronous).  The strategy
+ * is resolved once for the whole batch (every chunk runs it), so the result is
+ * bit-identical to rd_inverse_dynamics_f64 on the same batch.  Host calls on one
+ * model are serialised internally (the staging buffers are per model). */
 rd_status_t rd_inverse_dynamics_host_f64(rd_model_t m, int64_t batch, const double* q,
                                          const double* qd, const double* qdd, double* tau);
 /* Forward dynamics on HOST float64 arrays [n][batch] (same pipeline and rules as

@@ -31,7 +31,7 @@ FD_ALGOS = {"aba": 0, "jsiia": 1, "aba_scan": 2, "aba_merged": 3}
 
 # Symbols declared in include/rd.h (checked by tests/test_capi.py).
 EXPORTS = [
-    "rd_version", "rd_last_error", "rd_model_create", "rd_model_destroy", "rd_model_n",
+    "rd_version", "rd_last_error", "rd_model_create", "rd_model_destroy", "rd_model_n", "rd_model_device",
     "rd_model_set_strategy", "rd_model_resolve_strategy", "rd_model_set_boundary",
     "rd_inverse_dynamics_f64", "rd_inverse_dynamics_f32", "rd_forward_dynamics_f64",
     "rd_forward_dynamics_f32", "rd_model_set_fd_algo", "rd_inverse_dynamics_host_f64",
@@ -63,6 +63,8 @@ def lib():
         L.rd_model_destroy.argtypes = [vp]
         L.rd_model_n.argtypes = [vp]
         L.rd_model_n.restype = i32
+        L.rd_model_device.argtypes = [vp]
+        L.rd_model_device.restype = i32
         L.rd_model_set_strategy.argtypes = [vp, ctypes.c_int]
         L.rd_model_resolve_strategy.argtypes = [vp, i64, i32]
         L.rd_model_resolve_strategy.restype = ctypes.c_int
@@ -81,8 +83,8 @@ def lib():
         L.rd_forward_dynamics_host_f64.argtypes = [vp, i64, vp, vp, vp, vp]
         L.rd_last_launch_count.restype = i32
         for name in EXPORTS:
-            if name not in ("rd_version", "rd_last_error", "rd_model_n", "rd_model_resolve_strategy",
-                            "rd_last_launch_count"):
+            if name not in ("rd_version", "rd_last_error", "rd_model_n", "rd_model_device",
+                            "rd_model_resolve_strategy", "rd_last_launch_count"):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -119,6 +121,7 @@ class Model:
                "rd_model_create")
         self._h = h
         self.n = n
+        self.device = int(lib().rd_model_device(h))     # CUDA ordinal the constants live on
 
     @classmethod
     def from_robot(cls, robot: dict, gravity=(0.0, 0.0, -9.81)):
@@ -178,6 +181,8 @@ def _check_tensors(model: Model, *ts):
     if dt is not torch.float64 and dt is not torch.float32:
         raise RdError("dtype must be float64 or float32")
     dev = t0.get_device()
+    if dev != model.device:
+        raise RdError(f"tensors are on cuda:{dev} but the model was created on cuda:{model.device}")
     shape = t0.shape
     if len(shape) != 2 or shape[0] != model.n:
         raise RdError("tensors must be contiguous [n, B] with one dtype/device")
@@ -274,9 +279,16 @@ def _host_ptr(x):
 
 
 def _host_call(fn, name, model, a, b, c, out):
-    B = a.shape[1]
+    """Marshalling checks of the host-buffer API: four C-contiguous float64 host
+    arrays of one shape [n, B] (the library reads/writes n*B doubles of each)."""
+    if len(a.shape) != 2 or a.shape[0] != model.n:
+        raise RdError(f"host arrays must be [n, B] with n = {model.n}, got {tuple(a.shape)}")
     if out is None:
         out = np.empty_like(np.asarray(a)) if isinstance(a, np.ndarray) else a.new_empty(a.shape)
+    for x in (b, c, out):
+        if tuple(x.shape) != tuple(a.shape):
+            raise RdError(f"host arrays must share one shape {tuple(a.shape)}, got {tuple(x.shape)}")
+    B = a.shape[1]
     _check(fn(model.handle, B, _host_ptr(a), _host_ptr(b), _host_ptr(c), _host_ptr(out)), name)
     return out
 

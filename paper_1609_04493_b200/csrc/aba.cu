@@ -28,27 +28,14 @@
 
 namespace rd {
 
-#ifndef RD_ABA_WSPF
-#define RD_ABA_WSPF 2
-#endif
-// Input prefetch distances / unroll factors of the DH kernel's sweeps 1 and 3
-// (short iterations; see rnea_thread.cu StepCfg for why unroll ~ distance).
-#ifndef RD_ABA_MB
-#define RD_ABA_MB 3            // DH kernel: min CTAs of kAbaThreads per SM (register cap)
-#endif
-#ifndef RD_ABA_S1PD
-#define RD_ABA_S1PD 4
-#endif
-#ifndef RD_ABA_S1U
-#define RD_ABA_S1U 4
-#endif
-#ifndef RD_ABA_S3PD
-#define RD_ABA_S3PD 2          // re-measured after the sweep-2 trim: 2 / 2 0.4578 vs 1 / 2 0.4604 ms (C4)
-#endif
-#ifndef RD_ABA_S3U
-#define RD_ABA_S3U 2
-#endif
-constexpr int kS1PD = RD_ABA_S1PD, kS1U = RD_ABA_S1U, kS3PD = RD_ABA_S3PD, kS3U = RD_ABA_S3U;
+// Workspace read-ahead of sweep 3 (links), input prefetch distances / unroll
+// factors of the DH kernel's sweeps 1 and 3 (short iterations; see
+// rnea_thread.cu StepCfg for why unroll ~ distance), and the DH kernel's minimum
+// resident CTAs of kAbaThreads per SM (register cap).  Measured on B200, C4:
+// sweep-3 distance / unroll 2 / 2 0.4578 ms vs 1 / 2 0.4604 ms.
+constexpr int kWsPD = 2;
+constexpr int kAbaMinBlocks = 3;
+constexpr int kS1PD = 4, kS1U = 4, kS3PD = 2, kS3U = 2;
 constexpr int kAbaPerLink = 7;   // Ubar = U/D (6), ubar = u/D
 constexpr int kAbaThreads = 128;
 int aba_ws_per_link() { return kAbaPerLink; }
@@ -366,17 +353,15 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
         const int64_t o = (int64_t)min(j, n - 1) * B;
         bq[j] = __ldg(pq + o); bqd[j] = __ldg(pqd + o);
       }
-#if RD_ABA_WSPF
-      // (Ubar, ubar) of links i .. i+WSPF-1 in flight: the workspace reads come from
+      // (Ubar, ubar) of links i .. i+kWsPD-1 in flight: the workspace reads come from
       // DRAM (it does not fit in L2) and a sweep-3 step is short
-      constexpr int PD = RD_ABA_WSPF;
+      constexpr int PD = kWsPD;
       T cU[PD][7];
 #pragma unroll
       for (int j = 0; j < PD; ++j)
 #pragma unroll
         for (int k = 0; k < 7; ++k)
           cU[j][k] = (PR || k != 5) ? ws[((int64_t)min(j, n - 1) * kAbaPerLink + k) * slots + slot] : T(1);
-#endif
 #pragma unroll (kS3U)
       for (int i = 0; i < n; ++i) {
         const T cq3 = bq[0], cqd3 = bqd[0];
@@ -387,7 +372,6 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
           bq[kS3PD - 1] = __ldg(pq + o); bqd[kS3PD - 1] = __ldg(pqd + o);
         }
         const LinkDH<T>& C = L[i];
-#if RD_ABA_WSPF
         T Ub[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) Ub[k] = cU[0][k];
@@ -401,13 +385,6 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
 #pragma unroll
           for (int k = 0; k < 7; ++k) cU[PD - 1][k] = (PR || k != 5) ? wn[k * slots] : T(1);
         }
-#else
-        const T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
-        T Ub[6];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) Ub[k] = w[k * slots];
-        const T ub = w[6 * slots];
-#endif
         const bool pz = PR && PRs[i];
         const T qdi = cqd3;
         T Vn[6], an[6];
@@ -456,11 +433,11 @@ static cudaError_t launch_aba_dh_pr(int n, const LinkDH<T>* L_dev, const Boundar
   const int64_t grid = (ws_slots + kAbaThreads - 1) / kAbaThreads;
   const size_t smem = (size_t)n * sizeof(LinkDH<T>) + (PR ? (size_t)n : 0);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(aba_dh_kernel<T, RD_ABA_MB, PR, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(aba_dh_kernel<T, kAbaMinBlocks, PR, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  aba_dh_kernel<T, RD_ABA_MB, PR, SB><<<(unsigned)grid, kAbaThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws,
+  aba_dh_kernel<T, kAbaMinBlocks, PR, SB><<<(unsigned)grid, kAbaThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws,
                                                                           ws_slots, status, prism, sb);
   return cudaGetLastError();
 }

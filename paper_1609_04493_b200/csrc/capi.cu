@@ -167,15 +167,18 @@ struct rd_model_s {
   double sbAt[36] = {0};           // per-state boundary: user frame-n wrench -> kernel frame n
   rd::LinkConst<double>* dL64 = nullptr;
   rd::LinkConst<float>* dL32 = nullptr;
-  void* ws = nullptr;              // generic/FD workspace (device)
-  size_t ws_bytes = 0;
-  // host-buffer pipeline
+  // Workspace of the GENERIC ID and the FD kernels: allocated PER CALL, stream-ordered
+  // (cudaMallocFromPoolAsync before the launch, cudaFreeAsync after it, on the call's
+  // stream) from this model's memory pool, which keeps freed blocks cached (release
+  // threshold = max).  Concurrent calls on different streams therefore never share
+  // a workspace, and a call captured in a CUDA graph gets graph-owned memory.
+  cudaMemPool_t pool = nullptr;
+  std::mutex pool_mu;
+  // host-buffer pipeline (rd_*_host_f64): serialised by host_mu for the whole call
   void* hbuf[2] = {nullptr, nullptr};
   size_t hbuf_bytes = 0;
-  int64_t hchunk = 0;
   cudaStream_t hstream[2] = {nullptr, nullptr};
-  cudaEvent_t hevent[2] = {nullptr, nullptr};   // kernel-order chain across the two host streams
-  std::mutex mu;
+  std::mutex host_mu;
 };
 
 namespace {
@@ -344,37 +347,63 @@ bool build_dh(rd_model_t m, const std::vector<Rigid>& Mp, const std::vector<std:
   return true;
 }
 
-rd_status_t ensure_ws(rd_model_t m, size_t bytes) {
-  if (m->ws_bytes >= bytes) return RD_OK;
-  if (m->ws) cudaFree(m->ws);
-  m->ws = nullptr;
-  m->ws_bytes = 0;
-  cudaError_t e = cudaMalloc(&m->ws, bytes);
-  if (e != cudaSuccess) return fail(RD_E_NOMEM, std::string("workspace cudaMalloc: ") + cudaGetErrorString(e));
-  m->ws_bytes = bytes;
+// Stream-ordered workspace of one call (see rd_model_s::pool).  The pool is
+// created on first use on the model's device.
+rd_status_t ws_alloc(rd_model_t m, size_t bytes, cudaStream_t s, void** out) {
+  *out = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(m->pool_mu);
+    if (!m->pool) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = m->device;
+      cudaError_t e = cudaMemPoolCreate(&m->pool, &props);
+      if (e != cudaSuccess) { m->pool = nullptr; return cuda_fail(e, "workspace pool create"); }
+      uint64_t keep = UINT64_MAX;
+      e = cudaMemPoolSetAttribute(m->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      if (e != cudaSuccess) return cuda_fail(e, "workspace pool attribute");
+    }
+  }
+  cudaError_t e = cudaMallocFromPoolAsync(out, bytes, m->pool, s);
+  if (e != cudaSuccess) {
+    *out = nullptr;
+    return fail(RD_E_NOMEM, std::string("workspace cudaMallocFromPoolAsync: ") + cudaGetErrorString(e));
+  }
   return RD_OK;
 }
 
-// Device-memory check with a small per-thread cache of recently verified
-// pointers (cudaPointerGetAttributes costs ~1 us per pointer, which dominated the
-// host side of small-batch calls).  Safe under UVA: a device address is never a
-// valid host address, so a cached device pointer cannot later denote host memory.
-thread_local uintptr_t g_ptr_cache[16] = {0};
+// Frees the call's workspace on its stream after the launches (stream order).
+struct WsScope {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  ~WsScope() { if (p) cudaFreeAsync(p, s); }
+};
+
+// Device-memory check: the pointer must be device (or managed) memory of the
+// model's device.  A small per-thread cache of recently verified (address, device)
+// pairs skips cudaPointerGetAttributes (~1 us per pointer, which dominated the
+// host side of small-batch calls).  Under UVA an address denotes one allocation
+// at a time, so a cached device address cannot later denote host memory; a
+// freed and re-mapped address on ANOTHER device is the one case the cache can
+// miss, and it is re-verified whenever the cached device differs from the model's.
+struct PtrCacheEntry { uintptr_t addr; int device; };
+thread_local PtrCacheEntry g_ptr_cache[16] = {};
 thread_local int g_ptr_next = 0;
 
 template <typename T>
-bool is_device_ptr(const T* p) {
+bool is_device_ptr(const T* p, int device) {
   const uintptr_t a0 = reinterpret_cast<uintptr_t>(p);
-  for (uintptr_t c : g_ptr_cache)
-    if (c == a0) return true;
+  for (const PtrCacheEntry& c : g_ptr_cache)
+    if (c.addr == a0 && c.device == device) return true;
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  const bool dev = a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+  const bool dev = (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) && a.device == device;
   if (dev) {
-    g_ptr_cache[g_ptr_next] = a0;
+    g_ptr_cache[g_ptr_next] = PtrCacheEntry{a0, device};
     g_ptr_next = (g_ptr_next + 1) % 16;
   }
   return dev;
@@ -391,7 +420,8 @@ rd_status_t check_io(rd_model_t m, int64_t batch, const T* a, const T* b, const 
   for (int k = 0; k < 4; ++k) {
     if (!all[k]) return fail(RD_E_ARG, std::string("null pointer: ") + names[k]);
     if (reinterpret_cast<uintptr_t>(all[k]) % sizeof(T) != 0) return fail(RD_E_ARG, std::string("misaligned pointer: ") + names[k]);
-    if (device && !is_device_ptr(all[k])) return fail(RD_E_ARG, std::string("not device memory: ") + names[k]);
+    if (device && !is_device_ptr(all[k], m->device))
+      return fail(RD_E_ARG, std::string("not device memory of the model's device: ") + names[k]);
   }
   const size_t bytes = (size_t)m->n * (size_t)batch * sizeof(T);
   for (int k = 0; k < 3; ++k) {
@@ -487,7 +517,8 @@ rd_status_t check_state_boundary(rd_model_t m, int64_t batch, const UserStateBou
   for (int k = 0; k < 3; ++k) {
     if (!p[k]) continue;
     if (reinterpret_cast<uintptr_t>(p[k]) % sizeof(T) != 0) return fail(RD_E_ARG, std::string("misaligned pointer: ") + names[k]);
-    if (!is_device_ptr(reinterpret_cast<const T*>(p[k]))) return fail(RD_E_ARG, std::string("not device memory: ") + names[k]);
+    if (!is_device_ptr(reinterpret_cast<const T*>(p[k]), m->device))
+      return fail(RD_E_ARG, std::string("not device memory of the model's device: ") + names[k]);
     const char* lo = reinterpret_cast<const char*>(p[k]);
     const char* o = reinterpret_cast<const char*>(out);
     if (lo < o + ob && o < lo + bytes) return fail(RD_E_ARG, std::string("output aliases ") + names[k]);
@@ -505,14 +536,18 @@ void make_state_boundary(rd_model_t m, const UserStateBoundary& u, bool dh, rd::
   }
 }
 
+// force: the strategy resolved by the caller (the host pipeline resolves it ONCE for
+// the whole batch, so host and device results are bit-identical at any batch size);
+// RD_STRAT_AUTO = resolve here for this call's batch.
 template <typename T>
 rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* qd, const T* qdd, T* tau,
-                             void* stream, const UserStateBoundary* usb = nullptr) {
+                             void* stream, const UserStateBoundary* usb = nullptr,
+                             rd_strategy_t force = RD_STRAT_AUTO) {
   g_launches = 0;
   rd_status_t st = check_io<T>(m, batch, q, qd, qdd, tau, true);
   if (st != RD_OK || batch == 0) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  rd_strategy_t strat = resolve(m, batch, sizeof(T) == 8);
+  rd_strategy_t strat = force != RD_STRAT_AUTO ? force : resolve(m, batch, sizeof(T) == 8);
   rd::StateBoundary<T> sbj, sbd;                 // joint-frame / DH variants
   const rd::StateBoundary<T>* pj = nullptr;
   const rd::StateBoundary<T>* pd = nullptr;
@@ -559,12 +594,13 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
                                m->has_prism ? m->dPrism : nullptr, pd);
   }
   if (strat == RD_STRAT_GENERIC) {
-    std::lock_guard<std::mutex> lk(m->mu);
     const int64_t slots = rd::generic_ws_slots(batch);
-    st = ensure_ws(m, (size_t)slots * m->n * rd::generic_ws_per_link() * sizeof(T));
+    WsScope ws;
+    ws.s = s;
+    st = ws_alloc(m, (size_t)slots * m->n * rd::generic_ws_per_link() * sizeof(T), s, &ws.p);
     if (st != RD_OK) return st;
     e = rd::launch_rnea_generic<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau,
-                                   reinterpret_cast<T*>(m->ws), slots, s, &g_launches, pj);
+                                   reinterpret_cast<T*>(ws.p), slots, s, &g_launches, pj);
   }
   if (e != cudaSuccess) return cuda_fail(e, "inverse dynamics launch");
   return RD_OK;
@@ -578,7 +614,7 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   if (st != RD_OK || batch == 0) return st;
   if (status) {
     if (reinterpret_cast<uintptr_t>(status) % sizeof(int32_t) != 0) return fail(RD_E_ARG, "misaligned pointer: status");
-    if (!is_device_ptr(status)) return fail(RD_E_ARG, "not device memory: status");
+    if (!is_device_ptr(status, m->device)) return fail(RD_E_ARG, "not device memory of the model's device: status");
     const char* so = reinterpret_cast<const char*>(status);
     const char* qo = reinterpret_cast<const char*>(qdd);
     const size_t sb = (size_t)batch * sizeof(int32_t), qb = (size_t)m->n * (size_t)batch * sizeof(T);
@@ -593,14 +629,15 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     make_state_boundary<T>(m, *usb, false, &sbj);
     make_state_boundary<T>(m, *usb, true, &sbd);
   }
+  WsScope ws;                                       // this call's workspace, freed in stream order
+  ws.s = s;
   if (m->fd_algo == RD_FD_JSIIA) {
-    std::unique_lock<std::mutex> lk(m->mu, std::defer_lock);
+    if (m->n > 256) return fail(RD_E_UNSUPPORTED, "JSIIA forward dynamics supports n <= 256 (use RD_FD_ABA)");
     T* jws = nullptr;
-    if (m->n > 31) {                                  // CTA-wide JSIIA: per-CTA M in the model workspace
-      lk.lock();
-      st = ensure_ws(m, rd::jsiia_ws_elems(m->n, batch) * sizeof(T));
+    if (m->n > 31) {                                  // CTA-wide JSIIA: per-CTA M in the workspace
+      st = ws_alloc(m, rd::jsiia_ws_elems(m->n, batch) * sizeof(T), s, &ws.p);
       if (st != RD_OK) return st;
-      jws = reinterpret_cast<T*>(m->ws);
+      jws = reinterpret_cast<T*>(ws.p);
     }
     bool ok = false;
     cudaError_t e = rd::launch_jsiia<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd, s,
@@ -609,32 +646,33 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     if (e != cudaSuccess) return cuda_fail(e, "forward dynamics (JSIIA) launch");
     return RD_OK;
   }
-  std::lock_guard<std::mutex> lk(m->mu);
   if (m->fd_algo == RD_FD_ABA_SCAN || m->fd_algo == RD_FD_ABA_MERGED) {
-    st = ensure_ws(m, rd::fd_scan_ws_elems(m->n, batch) * sizeof(T));
+    const bool merged = m->fd_algo == RD_FD_ABA_MERGED;
+    if (merged ? m->n > 31 : m->n > 256)
+      return fail(RD_E_UNSUPPORTED, merged ? "merged-scan ABIA forward dynamics supports n <= 31 (use RD_FD_ABA)"
+                                           : "scan-ABIA forward dynamics supports n <= 256 (use RD_FD_ABA)");
+    st = ws_alloc(m, rd::fd_scan_ws_elems(m->n, batch) * sizeof(T), s, &ws.p);
     if (st != RD_OK) return st;
     bool ok = false;
-    const bool merged = m->fd_algo == RD_FD_ABA_MERGED;
     cudaError_t e = merged
         ? rd::launch_fd_merged<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
-                                  reinterpret_cast<T*>(m->ws), s, &g_launches, &ok, status)
+                                  reinterpret_cast<T*>(ws.p), s, &g_launches, &ok, status)
         : rd::launch_fd_scan<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
-                                reinterpret_cast<T*>(m->ws), s, &g_launches, &ok, status);
+                                reinterpret_cast<T*>(ws.p), s, &g_launches, &ok, status);
     if (!ok) return fail(RD_E_UNSUPPORTED, merged ? "merged-scan ABIA forward dynamics supports n <= 31 (use RD_FD_ABA)"
                                                   : "scan-ABIA forward dynamics supports n <= 256 (use RD_FD_ABA)");
     if (e != cudaSuccess) return cuda_fail(e, "forward dynamics (scan ABIA) launch");
     return RD_OK;
   }
   const int64_t slots = rd::generic_ws_slots(batch);
-  st = ensure_ws(m, (size_t)slots * m->n * rd::aba_ws_per_link() * sizeof(T));
+  st = ws_alloc(m, (size_t)slots * m->n * rd::aba_ws_per_link() * sizeof(T), s, &ws.p);
   if (st != RD_OK) return st;
-  static const bool no_dh = getenv("RD_ABA_NODH") && getenv("RD_ABA_NODH")[0] == '1';   // A/B knob
-  cudaError_t e = (m->dh_ok && !no_dh)
+  cudaError_t e = m->dh_ok
       ? rd::launch_aba_dh<T>(m->n, dh_dev<T>(m), dh_bnd<T>(m), batch, q, qd, tau, qdd,
-                             reinterpret_cast<T*>(m->ws), slots, s, &g_launches, status,
+                             reinterpret_cast<T*>(ws.p), slots, s, &g_launches, status,
                              m->has_prism ? m->dPrism : nullptr, usb ? &sbd : nullptr)
       : rd::launch_aba<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd,
-                          reinterpret_cast<T*>(m->ws), slots, s, &g_launches, status, usb ? &sbj : nullptr);
+                          reinterpret_cast<T*>(ws.p), slots, s, &g_launches, status, usb ? &sbj : nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "forward dynamics launch");
   return RD_OK;
 }
@@ -840,17 +878,17 @@ rd_status_t rd_model_destroy(rd_model_t m) {
   if (m->dC64) cudaFree(m->dC64);
   if (m->dC32) cudaFree(m->dC32);
   if (m->dPrism) cudaFree(m->dPrism);
-  if (m->ws) cudaFree(m->ws);
+  if (m->pool) cudaMemPoolDestroy(m->pool);
   for (int k = 0; k < 2; ++k) {
     if (m->hbuf[k]) cudaFree(m->hbuf[k]);
     if (m->hstream[k]) cudaStreamDestroy(m->hstream[k]);
-    if (m->hevent[k]) cudaEventDestroy(m->hevent[k]);
   }
   delete m;
   return RD_OK;
 }
 
 int32_t rd_model_n(rd_model_t m) { return m ? m->n : -1; }
+int32_t rd_model_device(rd_model_t m) { return m ? m->device : -1; }
 
 rd_status_t rd_model_set_strategy(rd_model_t m, rd_strategy_t s) {
   if (!m) return fail(RD_E_ARG, "null model");
@@ -933,35 +971,36 @@ rd_status_t rd_forward_dynamics_ex_f32(rd_model_t m, int64_t batch, const float*
   return forward_dynamics<float>(m, batch, q, qd, tau, qdd, stream, status);
 }
 
-// Host-buffer pipeline: chunks of `hchunk` states; chunk k uses device buffer
-// set k%2 and stream k%2: H2D(q,qd,qdd) -> kernel -> D2H(tau).  Two streams
-// overlap chunk k+1's copies with chunk k's kernel (PCIe is full duplex).
 }  // extern "C"
 
 namespace {
+// Host-buffer pipeline: chunks of `chunk` states; chunk k uses device buffer set
+// k%2 and stream k%2: H2D(q, qd, third) -> kernel -> D2H(out).  Two streams
+// overlap chunk k+1's copies with chunk k's kernel (PCIe is full duplex).  The
+// whole call holds the model's host_mu (the buffers and streams are per model),
+// and the ID strategy is resolved ONCE for the whole batch, so every chunk runs
+// the strategy a device call on the full batch would (bit-identical results).
 // FD: false = inverse dynamics (third input qdd, output tau), true = forward
 // dynamics (third input tau, output qdd; the model's FD algorithm).
+constexpr int64_t kHostChunkBytes = 32ll << 20;   // per input array; measured: 4/8/16/32/64 MB ->
+                                                  // 6.0/6.4/6.9/7.0/6.9e7 evals/s at C3 (PCIe-bound)
 template <bool FD>
 rd_status_t host_pipeline(rd_model_t m, int64_t batch, const double* q, const double* qd,
-                          const double* qdd, double* tau) {
+                          const double* third, double* out, int64_t chunk_bytes = kHostChunkBytes) {
   g_launches = 0;
-  rd_status_t st = check_io<double>(m, batch, q, qd, qdd, tau, false);
+  rd_status_t st = check_io<double>(m, batch, q, qd, third, out, false);
   if (st != RD_OK || batch == 0) return st;
   int dev = -1;
   cudaGetDevice(&dev);
   if (dev != m->device) return fail(RD_E_ARG, "current CUDA device differs from the model's device");
-  std::lock_guard<std::mutex> lk(m->mu);
+  std::lock_guard<std::mutex> lk(m->host_mu);
   const int n = m->n;
-  // chunk = ~32 MB of each input array (measured: 4/8/16/32/64 MB -> 6.0/6.4/6.9/7.0/6.9e7
-  // evals/s at C3, PCIe-bound at ~50 GB/s H2D): small enough that the pipeline fill/drain
-  // (first H2D, last kernel + D2H) is a few % of a 10^6-state call, large enough to amortise
-  // the per-copy overhead (RD_HOST_CHUNK_MB overrides, for measurement)
-  const char* env_chunk = getenv("RD_HOST_CHUNK_MB");
-  const int64_t chunk_mb = env_chunk ? std::max<int64_t>(1, atoll(env_chunk)) : 32;
-  const int64_t chunk = std::min<int64_t>(batch, std::max<int64_t>(4096, (chunk_mb << 20) / (8ll * n)));
+  const rd_strategy_t strat = FD ? RD_STRAT_AUTO : resolve(m, batch, true);
+  const int64_t chunk = std::min<int64_t>(batch, std::max<int64_t>(4096, chunk_bytes / (8ll * n)));
   const size_t set_bytes = (size_t)4 * n * chunk * sizeof(double);
   if (m->hbuf_bytes < set_bytes) {
     for (int k = 0; k < 2; ++k) {
+      if (m->hstream[k]) cudaStreamSynchronize(m->hstream[k]);
       if (m->hbuf[k]) cudaFree(m->hbuf[k]);
       m->hbuf[k] = nullptr;
     }
@@ -977,47 +1016,36 @@ rd_status_t host_pipeline(rd_model_t m, int64_t batch, const double* q, const do
       cudaError_t e = cudaStreamCreateWithFlags(&m->hstream[k], cudaStreamNonBlocking);
       if (e != cudaSuccess) return cuda_fail(e, "stream create");
     }
-    if (!m->hevent[k]) {
-      cudaError_t e = cudaEventCreateWithFlags(&m->hevent[k], cudaEventDisableTiming);
-      if (e != cudaSuccess) return cuda_fail(e, "event create");
-    }
   }
   int launches = 0;
+  rd_status_t result = RD_OK;
   for (int64_t b0 = 0, k = 0; b0 < batch; b0 += chunk, ++k) {
     const int64_t bc = std::min(chunk, batch - b0);
     cudaStream_t s = m->hstream[k & 1];
     double* base = reinterpret_cast<double*>(m->hbuf[k & 1]);
     double* dq = base;
     double* dqd = base + (size_t)n * chunk;
-    double* dqdd = base + (size_t)2 * n * chunk;
-    double* dtau = base + (size_t)3 * n * chunk;
+    double* d3 = base + (size_t)2 * n * chunk;
+    double* dout = base + (size_t)3 * n * chunk;
     const size_t hp = (size_t)batch * sizeof(double), dp = (size_t)bc * sizeof(double);
     cudaError_t e = cudaMemcpy2DAsync(dq, dp, q + b0, hp, dp, n, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemcpy2DAsync(dqd, dp, qd + b0, hp, dp, n, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemcpy2DAsync(dqdd, dp, qdd + b0, hp, dp, n, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return cuda_fail(e, "host path H2D");
-    // kernels run in chunk order: the kernels that use the model workspace
-    // (GENERIC ID, the FD algorithms) must not overlap across the two streams;
-    // the copies still overlap the neighbouring chunks' kernels
-    if (k > 0) e = cudaStreamWaitEvent(s, m->hevent[(k - 1) & 1], 0);
-    if (e != cudaSuccess) return cuda_fail(e, "host path event wait");
-    m->mu.unlock();
-    st = FD ? forward_dynamics<double>(m, bc, dq, dqd, dqdd, dtau, s)
-            : inverse_dynamics<double>(m, bc, dq, dqd, dqdd, dtau, s);
-    m->mu.lock();
+    if (e == cudaSuccess) e = cudaMemcpy2DAsync(d3, dp, third + b0, hp, dp, n, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) { result = cuda_fail(e, "host path H2D"); break; }
+    st = FD ? forward_dynamics<double>(m, bc, dq, dqd, d3, dout, s)
+            : inverse_dynamics<double>(m, bc, dq, dqd, d3, dout, s, nullptr, strat);
     launches += g_launches;
-    if (st != RD_OK) return st;
-    e = cudaEventRecord(m->hevent[k & 1], s);
-    if (e != cudaSuccess) return cuda_fail(e, "host path event record");
-    e = cudaMemcpy2DAsync(tau + b0, hp, dtau, dp, dp, n, cudaMemcpyDeviceToHost, s);
-    if (e != cudaSuccess) return cuda_fail(e, "host path D2H");
+    if (st != RD_OK) { result = st; break; }
+    e = cudaMemcpy2DAsync(out + b0, hp, dout, dp, dp, n, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) { result = cuda_fail(e, "host path D2H"); break; }
   }
+  // always drain both streams before releasing the lock (the buffers are reused)
   for (int k = 0; k < 2; ++k) {
     cudaError_t e = cudaStreamSynchronize(m->hstream[k]);
-    if (e != cudaSuccess) return cuda_fail(e, "host path sync");
+    if (e != cudaSuccess && result == RD_OK) result = cuda_fail(e, "host path sync");
   }
   g_launches = launches;
-  return RD_OK;
+  return result;
 }
 }  // namespace
 

@@ -23,19 +23,11 @@ constexpr int kRevThreads = 128;
 // distance keeps the in-flight loads in fixed registers (no MOV rotation that
 // waits on them at every loop head); tau is stored one link late, off the end
 // of the backward DFMA chain (thread kernel).
-#ifndef RD_REV_PD
-#define RD_REV_PD 4
-#endif
-#ifndef RD_REV_U
-#define RD_REV_U 4
-#endif
-#ifndef RD_REV_MB
-#define RD_REV_MB 4
-#endif
-constexpr int kRevPD = RD_REV_PD, kRevU = RD_REV_U;
+constexpr int kRevPD = 4, kRevU = 4;
+constexpr int kRevMinBlocks = 4;   // resident CTAs per SM (128-register cap)
 
 template <typename T, bool PR, bool SB>
-__global__ void __launch_bounds__(kRevThreads, RD_REV_MB)
+__global__ void __launch_bounds__(kRevThreads, kRevMinBlocks)
 rnea_rev_kernel(int n, const LinkDHc<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
                 const T* __restrict__ q, const T* __restrict__ qd, const T* __restrict__ qdd,
                 T* __restrict__ tau, const unsigned char* __restrict__ prism_g,
@@ -160,7 +152,7 @@ static cudaError_t launch_rev(int n, const LinkDHc<T>* L_dev, const Boundary<T>&
     if (e != cudaSuccess) return e;
   }
   int64_t grid = (B + kRevThreads - 1) / kRevThreads;
-  const int64_t cap = (int64_t)num_sms() * RD_REV_MB;
+  const int64_t cap = (int64_t)num_sms() * kRevMinBlocks;
   if (grid > cap) grid = cap;
   rnea_rev_kernel<T, PR, SB><<<(unsigned)grid, kRevThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, qdd, tau, prism,
                                                                          sb);

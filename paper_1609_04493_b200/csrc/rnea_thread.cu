@@ -132,49 +132,22 @@ template <> struct TmemIO<float> {
 // B200: fp64 n = 30 (W = 8), 1M states 0.543 -> 0.494 ms with
 // (8, 4); fp32 n = 30 (W = 16) 0.312 -> 0.309 ms with (4, 2); the 16-warp fp64
 // plan (n <= 15, 128-register cap) also (4, 2): n = 15, 1M 0.227 -> 0.222 ms.
-#ifndef RD_PD64
-#define RD_PD64 8
-#endif
-#ifndef RD_U64
-#define RD_U64 4
-#endif
-#ifndef RD_PD32
-#define RD_PD32 4
-#endif
-#ifndef RD_U32
-#define RD_U32 2
-#endif
-#ifndef RD_TAU_DEFER
-#define RD_TAU_DEFER 1
-#endif
-#ifndef RD_STASH_VEC
-#define RD_STASH_VEC 1
-#endif
 // kFwdFirst: issue the forward link before the backward one in a step (fp32 -3 %,
 // fp64 +5 %, measured).
-#ifndef RD_PD64W16
-#define RD_PD64W16 4
-#endif
-#ifndef RD_U64W16
-#define RD_U64W16 2
-#endif
-template <typename T, int W> struct StepCfg {
-  static constexpr int kPD = RD_PD64W16, kUnroll = RD_U64W16;
+template <typename T, int W> struct StepCfg {       // fp64, W = 16 (n <= 15, 128 registers)
+  static constexpr int kPD = 4, kUnroll = 2;
   static constexpr bool kFwdFirst = false;
 };
-#ifndef RD_FWDFIRST64
-#define RD_FWDFIRST64 0
-#endif
 template <> struct StepCfg<double, 8> {
-  static constexpr int kPD = RD_PD64, kUnroll = RD_U64;
-  static constexpr bool kFwdFirst = RD_FWDFIRST64;
+  static constexpr int kPD = 8, kUnroll = 4;
+  static constexpr bool kFwdFirst = false;
 };
 template <> struct StepCfg<float, 8> {
-  static constexpr int kPD = RD_PD32, kUnroll = RD_U32;
+  static constexpr int kPD = 4, kUnroll = 2;
   static constexpr bool kFwdFirst = true;
 };
 template <> struct StepCfg<float, 16> {
-  static constexpr int kPD = RD_PD32, kUnroll = RD_U32;
+  static constexpr int kPD = 4, kUnroll = 2;
   static constexpr bool kFwdFirst = true;
 };
 
@@ -194,10 +167,8 @@ struct BwdState {
   T ca, sa, a, d, s, c;         // DH constants and stashed (sin, cos) of the child link i+1
   int64_t b;
   bool valid;
-#if RD_TAU_DEFER
   T tp;                         // tau of the previous backward link, stored one step later
   int ip;                       // its link index (-1: none pending)
-#endif
 };
 
 // fp32 runs the per-link algebra on packed pairs (FFMA2 / FMUL2, sm_100a f32x2):
@@ -340,16 +311,12 @@ __device__ __forceinline__ void fwd_init(FwdState<T, PD>& f, const ThreadParams<
 }
 template <typename T>
 __device__ __forceinline__ void bwd_flush(BwdState<T>& g, int64_t B, T* __restrict__ tau) {
-#if RD_TAU_DEFER
   if (g.valid && g.ip >= 0) tau[(int64_t)g.ip * B + g.b] = g.tp;
   g.ip = -1;
-#endif
 }
 template <typename T>
 __device__ __forceinline__ void bwd_init(BwdState<T>& g, const ThreadParams<T>& P) {
-#if RD_TAU_DEFER
   g.ip = -1;
-#endif
 #pragma unroll
   for (int k = 0; k < 6; ++k) g.F[k] = P.bnd.Ftip[k];
   if constexpr (kPacked<T>) {
@@ -450,11 +417,9 @@ template <bool PR, typename T>
 __device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& P, int64_t B, int i,
                                          const T* cur, T* __restrict__ tau) {
   T Fo[6];
-#if RD_TAU_DEFER
   // the previous link's tau, whose DFMA chain finished a whole step ago (storing
   // it right after the chain stalled the warp on the fixed-latency dependency)
   if (g.valid && g.ip >= 0) tau[(int64_t)g.ip * B + g.b] = g.tp;
-#endif
   const LinkDHc<T>& C = P.L[i];
   const bool prism = PR && ((P.prism >> i) & 1u);
   T ti;                                            // tau_i = S_i^T F_i
@@ -467,12 +432,8 @@ __device__ __forceinline__ void bwd_link(BwdState<T>& g, const ThreadParams<T>& 
     for (int j = 0; j < 6; ++j) g.F[j] = Fo[j];
     ti = prism ? g.F[2] : g.F[5];
   }
-#if RD_TAU_DEFER
   g.tp = ti;
   g.ip = i;
-#else
-  if (g.valid) tau[(int64_t)i * B + g.b] = ti;
-#endif
   g.ca = C.ca; g.sa = C.sa; g.a = C.a;
   if (PR) {
     g.d = prism ? C.d + cur[0] : C.d;               // prismatic: d = d0 + q
@@ -504,7 +465,6 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
   const int n = P.n, lt = P.lt;
   const int64_t ntiles = (B + NT - 1) / NT;
   const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-#if RD_STASH_VEC
   // 16-byte vectors: [slot - lt][8 / VW][NT] of (double2 | float4) -- conflict-free
   // (consecutive threads 16 B apart), 2 (fp32) / 4 (fp64) shared-memory
   // instructions per slot instead of 8 (the fp32 kernel is issue-bound)
@@ -533,20 +493,6 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
       for (int j = 0; j < VW; ++j) cur[k * VW + j] = e[j];
     }
   };
-#else
-  T* sstash = reinterpret_cast<T*>(smem_raw);     // slots lt..n-1: [slot - lt][8][NT]
-  auto sptr = [&](int slot) { return sstash + (size_t)(slot - lt) * 8 * NT + tid; };
-  auto put_smem = [&](int slot, const T* st) {
-    T* d = sptr(slot);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) d[k * NT] = st[k];
-  };
-  auto get_smem = [&](int slot, T* cur) {
-    const T* d = sptr(slot);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) cur[k] = d[k * NT];
-  };
-#endif
   auto put_any = [&](int slot, const T* st) {
     if (slot < lt) TmemIO<T>::st(tbase + (uint32_t)(slot * KC), st);
     else put_smem(slot, st);
@@ -567,9 +513,7 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
   BwdState<T> g;
   g.b = 0;
   g.valid = false;
-#if RD_TAU_DEFER
   g.ip = -1;
-#endif
   for (int64_t it = 0; it <= my_tiles; ++it) {
     const int64_t b = (blockIdx.x + it * gridDim.x) * NT + tid;
     const bool fvalid = b < B;

@@ -234,3 +234,64 @@ def robot_for(cfg: dict):
     if cfg["robot"] == "arm7":
         return arm7()
     return random_chain(cfg["n"], 1000 + cfg["n"])
+
+
+# ---------------------------------------------------------------------------
+# The same state generator on the GPU (synth/gen.cu -> synth/libsynth.so):
+# each rank generates its shard in device memory from the GLOBAL state indices.
+# ---------------------------------------------------------------------------
+
+import ctypes as _ctypes  # noqa: E402
+import os as _os  # noqa: E402
+import subprocess as _subprocess  # noqa: E402
+
+_HERE = _os.path.dirname(_os.path.abspath(__file__))
+_GEN_SRC = _os.path.join(_HERE, "gen.cu")
+_GEN_LIB = _os.path.join(_HERE, "libsynth.so")
+_gen = None
+
+
+def build_device_generator(force: bool = False) -> str:
+    """nvcc -> synth/libsynth.so (sm_100a), if missing or older than gen.cu."""
+    if force or not _os.path.exists(_GEN_LIB) or _os.path.getmtime(_GEN_LIB) < _os.path.getmtime(_GEN_SRC):
+        nvcc = "/usr/local/cuda/bin/nvcc" if _os.path.exists("/usr/local/cuda/bin/nvcc") else "nvcc"
+        tmp = _GEN_LIB + f".tmp{_os.getpid()}"
+        _subprocess.check_call([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
+                                "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-o", tmp, _GEN_SRC])
+        _os.replace(tmp, _GEN_LIB)
+    return _GEN_LIB
+
+
+def _gen_lib():
+    global _gen
+    if _gen is None:
+        build_device_generator()
+        L = _ctypes.CDLL(_GEN_LIB)
+        u64, i32, i64, dbl, vp = (_ctypes.c_uint64, _ctypes.c_int, _ctypes.c_int64, _ctypes.c_double,
+                                  _ctypes.c_void_p)
+        for name in ("synth_uniform_states_f64", "synth_uniform_states_f32"):
+            getattr(L, name).argtypes = [u64, i32, i32, i64, i64, dbl, dbl, vp, i64, vp]
+            getattr(L, name).restype = i32
+        _gen = L
+    return _gen
+
+
+def states_device(seed: int, n: int, b0: int, b1: int, ranges: str = "default", dtype=None, device=None):
+    """`states` generated on the GPU: (q, qd, qdd) torch tensors [n, b1-b0] of
+    `dtype` (float64 default; float32 = the float64 draw rounded to nearest)
+    on `device`, bit-identical to torch.from_numpy(states(...)).to(dtype)."""
+    import torch
+    dtype = torch.float64 if dtype is None else dtype
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    L = _gen_lib()
+    fn = L.synth_uniform_states_f64 if dtype == torch.float64 else L.synth_uniform_states_f32
+    out = []
+    with torch.cuda.device(device):
+        stream = torch.cuda.current_stream(device).cuda_stream
+        for k, (lo, hi) in enumerate(_RANGES[ranges]):
+            t = torch.empty((n, b1 - b0), dtype=dtype, device=device)
+            rc = fn(seed & 0xFFFFFFFFFFFFFFFF, k, n, b0, b1, float(lo), float(hi), t.data_ptr(), b1 - b0, stream)
+            if rc:
+                raise RuntimeError(f"synth device generator failed (status {rc})")
+            out.append(t)
+    return tuple(out)

@@ -17,6 +17,22 @@ pytestmark = pytest.mark.gpu
 TOL = {torch.float64: 1e-10, torch.float32: 1e-4}
 
 
+def parity_sample(B, tile=256, seed=99):
+    """SURVEY §8(d) parity sample of a B-state launch: the first and last 1024
+    states, both neighbours of EVERY tile boundary of the thread kernel (tiles of
+    `tile` = 32 W states, W = 8 fp64 / 16 fp32, so 256 covers both), every shard
+    boundary of k = 2, 4, 8 ranks +-16, and 65,536 random indices (seed 99)."""
+    rng = np.random.default_rng(seed)
+    parts = [np.arange(min(B, 1024)), np.arange(max(0, B - 1024), B), rng.integers(0, B, 65536)]
+    edges = np.arange(tile, B, tile)
+    parts += [edges - 1, edges]
+    for k in (2, 4, 8):
+        for r in range(1, k):
+            b = (B // k) * r + min(r, B % k)
+            parts.append(np.arange(max(0, b - 16), min(B, b + 16)))
+    return np.unique(np.concatenate(parts))
+
+
 @pytest.fixture(scope="module")
 def rd():
     if not torch.cuda.is_available():
@@ -74,9 +90,8 @@ def test_C3_full_size_sampled(rd, dtype):
     cfg = synth.CONFIGS["C3"]
     n, B = cfg["n"], cfg["batch"]
     q, qd, qdd = synth.states(cfg["seed"], n, 0, B, cfg["ranges"])
-    rng = np.random.default_rng(99)
-    sample = np.unique(np.concatenate([np.arange(1024), np.arange(B - 1024, B),
-                                       rng.integers(0, B, 8192), np.arange(127, B, 128 * 997)]))
+    sample = parity_sample(B)
+    assert sample.size >= 65536
     check_id(rd, synth.robot_for(cfg), cfg["gravity"], q, qd, qdd, dtype, sample=sample)
 
 
@@ -96,9 +111,8 @@ def test_C5_full_size_sampled(rd):
     model = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
     assert model.resolve_strategy(B, True) == "thread"
     tau = rd.inverse_dynamics(model, tq, tqd, tqdd)
-    rng = np.random.default_rng(99)
-    sample = np.unique(np.concatenate([np.arange(512), np.arange(B - 512, B), rng.integers(0, B, 4096),
-                                       np.arange(255, B, 256 * 9973), np.arange(256, B, 256 * 9973)]))
+    sample = parity_sample(B)
+    assert sample.size >= 65536
     idx = torch.from_numpy(sample).cuda()
     got = tau[:, idx].cpu().numpy()
     q, qd, qdd = (t[:, idx].cpu().numpy() for t in (tq, tqd, tqdd))
@@ -268,6 +282,11 @@ def test_full_boundary_V0_Vdot0_Ftip(rd):
         assert rel_err_per_state(tau, ref).max() <= 1e-10
 
 
+def _rounded(x, dtype):
+    """x as the kernel sees it: rounded to fp32 for the fp32 path (A15)."""
+    return x.astype(np.float32).astype(np.float64) if dtype == torch.float32 else x
+
+
 def _per_state_boundary(rng, B, which):
     arrs = [rng.standard_normal((6, B)) if w else None for w in which]
     return arrs
@@ -283,10 +302,11 @@ def test_per_state_boundary_id(rd, dtype, kind):
         i = int(np.argmax(np.linalg.norm(r["S"][:, 3:], axis=1)))
         r["S"][i, :3] += 0.2 * r["S"][i, 3:]
     rng = np.random.default_rng(7)
-    q, qd, qdd = synth.states(16, n, 0, B)
+    # the oracle sees exactly the (fp32-rounded) inputs the kernel sees (A15)
+    q, qd, qdd = (_rounded(x, dtype) for x in synth.states(16, n, 0, B))
     model = rd.Model.from_robot(r, synth.GRAVITY_Z)
     for which in ((1, 1, 1), (0, 0, 1), (1, 0, 0)):
-        V0, Vd0, Ft = _per_state_boundary(rng, B, which)
+        V0, Vd0, Ft = (None if a is None else _rounded(a, dtype) for a in _per_state_boundary(rng, B, which))
         gv0, gvd0, gft = oracle.gravity_boundary(synth.GRAVITY_Z)   # the model's values (A3)
         ref = np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b],
                                     V0=gv0 if V0 is None else V0[:, b],
@@ -297,8 +317,8 @@ def test_per_state_boundary_id(rd, dtype, kind):
             model.set_strategy(strat)
             tau = rd.inverse_dynamics(model, dev(q, dtype), dev(qd, dtype), dev(qdd, dtype),
                                       boundary=bnd).double().cpu().numpy()
-            tol = 1e-10 if dtype == torch.float64 else 2e-4
-            assert rel_err_per_state(tau, ref).max() <= tol, (strat, which)
+            err = rel_err_per_state(tau, ref).max()
+            assert err <= TOL[dtype], (strat, which, err)
     model.set_strategy("warp_scan_eq13")
     with pytest.raises(rd.RdError):
         rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd), boundary=(None, None, dev(np.zeros((6, B)))))
@@ -355,23 +375,84 @@ def test_host_path_equals_device_path(rd):
     np.testing.assert_array_equal(out.numpy(), dev_tau)
 
 
-def test_host_path_multichunk_workspace_kernels(rd, monkeypatch):
-    # small chunks: many chunks alternate between the two host streams; GENERIC ID
-    # (screw joint) and the FD algorithms share the model workspace across chunks
-    monkeypatch.setenv("RD_HOST_CHUNK_MB", "1")
-    r = synth.random_chain(10, 1313, prismatic_fraction=0.3)
+def test_host_path_multichunk_bit_identical(rd):
+    # 1M states at n = 30 is 8 host chunks (32 MB per input array each) with a ragged
+    # last chunk; the strategy is resolved once for the whole batch, so the host path
+    # equals the device path bit for bit (every chunk runs THREAD)
+    cfg = synth.CONFIGS["C3"]
+    n, B = 30, 1_000_000
+    model = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
+    assert model.resolve_strategy(B, True) == "thread"
+    q, qd, qdd = synth.states(cfg["seed"], n, 0, B)
+    dev_tau = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd)).cpu().numpy()
+    pq, pqd, pqdd = (torch.from_numpy(x).pin_memory() for x in (q, qd, qdd))
+    out = torch.empty_like(pq).pin_memory()
+    rd.inverse_dynamics_host(model, pq, pqd, pqdd, out)
+    np.testing.assert_array_equal(out.numpy(), dev_tau)
+    with pytest.raises(rd.RdError):                      # shape checks of the host binding
+        rd.inverse_dynamics_host(model, q[:, :10], qd, qdd)
+    with pytest.raises(rd.RdError):
+        rd.inverse_dynamics_host(model, q, qd, qdd, np.empty((n, B - 1)))
+
+
+def test_host_path_multichunk_workspace_kernels(rd):
+    # n = 60: a chunk is 69,905 states, so 150,000 states are 3 chunks alternating
+    # between the two host streams; GENERIC ID (screw joint) and every FD algorithm
+    # allocate their workspace per call (stream-ordered) on those streams
+    n, B = 60, 150_000
+    r = synth.random_chain(n, 1313, prismatic_fraction=0.3)
     i = int(np.argmax(np.linalg.norm(r["S"][:, 3:], axis=1)))
     r["S"][i, :3] += 0.2 * r["S"][i, 3:]                    # screw joint -> GENERIC / joint-frame ABA
-    q, qd, qdd = synth.states(18, 10, 0, 60000)
+    q, qd, qdd = synth.states(18, n, 0, B)
     model = rd.Model.from_robot(r, synth.GRAVITY_Z)
+    assert model.resolve_strategy(B, True) == "generic"
     dev_tau = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd)).cpu().numpy()
     np.testing.assert_array_equal(rd.inverse_dynamics_host(model, q, qd, qdd), dev_tau)
+    sub = np.arange(0, B, 997)
     for algo in ("aba", "jsiia", "aba_scan"):
         model.set_fd_algo(algo)
         dev_qdd = rd.forward_dynamics(model, dev(q), dev(qd), dev(dev_tau)).cpu().numpy()
         host_qdd = rd.forward_dynamics_host(model, q, qd, dev_tau)
         np.testing.assert_array_equal(host_qdd, dev_qdd)
-        assert rel_err_per_state(host_qdd, qdd, floor=1.0).max() < 1e-8
+        back = oracle.rnea_batch(r, synth.GRAVITY_Z, q[:, sub], qd[:, sub], host_qdd[:, sub])
+        assert rel_err_per_state(back, dev_tau[:, sub]).max() <= 1e-10
+
+
+def test_concurrent_streams_share_no_workspace(rd):
+    # two streams run GENERIC ID (per-call workspace) and ABA FD on ONE model at the
+    # same time, with different inputs; each result equals its serial run
+    n = 24
+    r = synth.random_chain(n, 1414, prismatic_fraction=0.3)
+    i = int(np.argmax(np.linalg.norm(r["S"][:, 3:], axis=1)))
+    r["S"][i, :3] += 0.2 * r["S"][i, 3:]                    # screw joint -> GENERIC ID
+    model = rd.Model.from_robot(r, synth.GRAVITY_Z)
+    model.set_strategy("generic")
+    B = 200_000
+    ins = [tuple(dev(x) for x in synth.states(30 + k, n, 0, B)) for k in range(2)]
+    ref_id = [rd.inverse_dynamics(model, *x) for x in ins]
+    ref_fd = [rd.forward_dynamics(model, x[0], x[1], t) for x, t in zip(ins, ref_id)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    for rep in range(3):
+        outs_id = [torch.empty_like(ins[0][0]) for _ in range(2)]
+        outs_fd = [torch.empty_like(ins[0][0]) for _ in range(2)]
+        for k, s in enumerate(streams):
+            s.wait_stream(torch.cuda.current_stream())
+            rd.inverse_dynamics(model, *ins[k], out=outs_id[k], stream=s)
+            rd.forward_dynamics(model, ins[k][0], ins[k][1], ref_id[k], out=outs_fd[k], stream=s)
+        torch.cuda.synchronize()
+        for k in range(2):
+            assert torch.equal(outs_id[k], ref_id[k]), (rep, k)
+            assert torch.equal(outs_fd[k], ref_fd[k]), (rep, k)
+
+
+def test_device_mismatch_rejected(rd):
+    if torch.cuda.device_count() < 2:
+        pytest.skip("one GPU: the cross-device check needs two")
+    model = rd.Model.from_robot(synth.random_chain(6, 1), synth.GRAVITY_Z)
+    z = torch.zeros((6, 10), dtype=torch.float64, device="cuda:1")
+    with pytest.raises(rd.RdError):
+        rd.inverse_dynamics(model, z, z, z)
 
 
 def test_launch_count_and_errors(rd):
@@ -386,29 +467,54 @@ def test_launch_count_and_errors(rd):
 
 
 # ------------------------------------------------------------------ forward dynamics (ABA)
-def check_fd(rd, robot, g, B, seed, dtype=torch.float64, bwd_tol=1e-10):
+def cond_forward_check(robot, g, q, qd, tau, out, ref, sample):
+    """Cond-scaled forward error (A14) on sampled states.  tau(qdd) = M(q) qdd + h is
+    affine, so for the GPU answer `out` and the oracle's `ref`
+        M (out - ref) = r_gpu - r_orc,   r = RNEA(q, qd, qdd_x) - tau,
+    hence ||out - ref||_2 <= (||r_gpu||_2 + ||r_orc||_2 + eval rounding) / lambda_min(M):
+    the forward error is fully explained by the two backward errors times
+    ||M^-1|| (cond(M) / ||M||).  Returns the sampled cond(M) values."""
+    qs, qds, ts, os_, rs = (x[:, sample] for x in (q, qd, tau, out, ref))
+    r_gpu = oracle.rnea_batch(robot, g, qs, qds, os_) - ts
+    r_orc = oracle.rnea_batch(robot, g, qs, qds, rs) - ts
+    conds = []
+    for k in range(len(sample)):
+        lam = np.linalg.eigvalsh(oracle.jsi(robot, qs[:, k]))
+        assert lam[0] > 0
+        conds.append(lam[-1] / lam[0])
+        rnd = 1e-12 * (np.linalg.norm(ts[:, k]) + lam[-1] * np.linalg.norm(rs[:, k]))
+        bound = (np.linalg.norm(r_gpu[:, k]) + np.linalg.norm(r_orc[:, k]) + rnd) / lam[0]
+        fe = np.linalg.norm(os_[:, k] - rs[:, k])
+        assert fe <= 1.5 * bound, (sample[k], fe, bound, conds[-1])
+    return np.array(conds)
+
+
+def check_fd(rd, robot, g, B, seed, dtype=torch.float64, bwd_tol=None, n_cond=48):
+    """FD parity (A14): backward error ||RNEA(q, qd, qdd_gpu) - tau|| / ||tau|| per state
+    <= the contract tolerance (1e-10 fp64, 1e-4 fp32), plus the cond-scaled forward
+    error of `cond_forward_check` on n_cond sampled states.  Returns (max backward
+    error, max forward error, max sampled cond(M))."""
     n = robot["S"].shape[0]
-    q, qd, qdd = synth.states(seed, n, 0, B)
-    if dtype == torch.float32:
-        q, qd, qdd = (x.astype(np.float32).astype(np.float64) for x in (q, qd, qdd))
-    tau = oracle.rnea_batch(robot, g, q, qd, qdd)
-    if dtype == torch.float32:
-        tau = tau.astype(np.float32).astype(np.float64)
+    q, qd, qdd = (_rounded(x, dtype) for x in synth.states(seed, n, 0, B))
+    tau = _rounded(oracle.rnea_batch(robot, g, q, qd, qdd), dtype)
     model = rd.Model.from_robot(robot, g)
     out = rd.forward_dynamics(model, dev(q, dtype), dev(qd, dtype), dev(tau, dtype)).double().cpu().numpy()
     assert np.all(np.isfinite(out))
     back = oracle.rnea_batch(robot, g, q, qd, out)       # backward error (A14)
     berr = rel_err_per_state(back, tau)
-    assert berr.max() <= bwd_tol, f"FD backward error {berr.max():.3e}"
+    tol = TOL[dtype] if bwd_tol is None else bwd_tol
+    assert berr.max() <= tol, f"FD backward error {berr.max():.3e}"
     fwd = oracle.fd_batch(robot, g, q, qd, tau)
     ferr = rel_err_per_state(out, fwd, floor=1.0)
-    return berr.max(), ferr.max()
+    sample = np.unique(np.linspace(0, B - 1, min(B, n_cond)).astype(np.int64))
+    conds = cond_forward_check(robot, g, q, qd, tau, out, fwd, sample)
+    return berr.max(), ferr.max(), conds.max()
 
 
 @pytest.mark.parametrize("n", [1, 2, 7, 30])
 def test_fd_aba_parity(rd, n):
     r = synth.random_chain(n, 900 + n, prismatic_fraction=0.3 if n < 30 else 0.0)
-    b, f = check_fd(rd, r, synth.GRAVITY_Z, 2000, 4)
+    b, f, c = check_fd(rd, r, synth.GRAVITY_Z, 2000, 4)
     assert f < 1e-8
 
 
@@ -416,7 +522,7 @@ def test_fd_aba_parity(rd, n):
 def test_fd_aba_prismatic_dh(rd, n, pf):
     # revolute + prismatic chains take the DH-frame ABA (prismatic instantiation)
     r = synth.random_chain(n, 930 + n, prismatic_fraction=pf)
-    b, f = check_fd(rd, r, synth.GRAVITY_Z, 1500, 6)       # backward error <= 1e-10 inside (A14)
+    b, f, c = check_fd(rd, r, synth.GRAVITY_Z, 1500, 6)    # backward error <= 1e-10 inside (A14)
     assert f < 1e-5                                        # forward error: cond(M)-limited (A14)
 
 
@@ -427,9 +533,9 @@ def test_fd_aba_screw_joints_joint_frames(rd):
         if np.linalg.norm(r["S"][i, 3:]) > 0.5:
             r["S"][i, :3] += 0.15 * r["S"][i, 3:]
             break
-    b, f = check_fd(rd, r, synth.GRAVITY_Z, 1500, 7)
+    b, f, c = check_fd(rd, r, synth.GRAVITY_Z, 1500, 7)
     assert f < 1e-7
-    b32, _ = check_fd(rd, r, synth.GRAVITY_Z, 500, 8, torch.float32, bwd_tol=1e-3)
+    check_fd(rd, r, synth.GRAVITY_Z, 500, 8, torch.float32)   # fp32: backward error <= 1e-4
 
 
 def test_fd_C4_sampled(rd):
@@ -451,7 +557,7 @@ def test_fd_C4_sampled(rd):
 
 def test_fd_fp32(rd):
     r = synth.random_chain(7, 907)
-    check_fd(rd, r, synth.GRAVITY_Z, 2000, 5, torch.float32, bwd_tol=1e-4)
+    check_fd(rd, r, synth.GRAVITY_Z, 2000, 5, torch.float32)
 
 
 def test_fd_pendulum_closed_form(rd):
@@ -513,6 +619,7 @@ def test_fd_jsiia_parity(rd, n, pf):
     assert rel_err_per_state(back, tau).max() <= 1e-10
     ref = oracle.fd_batch(r, g, q, qd, tau, algo="jsiia")
     assert rel_err_per_state(out, ref, floor=1.0).max() < (1e-7 if n <= 31 else 1e-5)   # cond(M), A14
+    cond_forward_check(r, g, q, qd, tau, out, ref, np.arange(0, 1500, 50))
 
 
 def test_fd_jsiia_boundary_and_limits(rd):
@@ -550,6 +657,7 @@ def test_fd_aba_scan_parity(rd, n, pf):
     ref = oracle.fd_batch(r, g, q, qd, tau)
     # forward error is cond(M)-limited (A14): cond grows fast with n
     assert rel_err_per_state(out, ref, floor=1.0).max() < (1e-7 if n <= 32 else 1e-5)
+    cond_forward_check(r, g, q, qd, tau, out, ref, np.arange(0, 1500, 50))
     assert rd.last_launch_count() == 3
 
 
@@ -569,6 +677,7 @@ def test_fd_aba_merged_parity(rd, n, pf):
     sub = np.arange(0, 1200, 37)                                # the oracle's literal Eq. (20) path
     ref = oracle.fd_batch(r, g, q[:, sub], qd[:, sub], tau[:, sub], algo="aba_merged")
     assert rel_err_per_state(out[:, sub], ref, floor=1.0).max() < 1e-7
+    cond_forward_check(r, g, q[:, sub], qd[:, sub], tau[:, sub], out[:, sub], ref, np.arange(sub.size))
     assert rd.last_launch_count() == 3
 
 
@@ -585,9 +694,12 @@ def test_fd_scan_variants_boundary_fp32_limits(rd, algo):
     tau = np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b], V0, Vd0, Ft) for b in range(257)], 1)
     out = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()
     assert rel_err_per_state(out, qdd, floor=1.0).max() < 1e-9
-    out32 = rd.forward_dynamics(model, dev(q, torch.float32), dev(qd, torch.float32),
-                                dev(tau, torch.float32)).cpu().numpy()
-    assert rel_err_per_state(out32, qdd, floor=1.0).max() < 1e-3
+    # fp32 (A15): the oracle sees the fp32-rounded inputs; backward error <= 1e-4
+    q32, qd32, t32 = (_rounded(x, torch.float32) for x in (q, qd, tau))
+    out32 = rd.forward_dynamics(model, dev(q32, torch.float32), dev(qd32, torch.float32),
+                                dev(t32, torch.float32)).double().cpu().numpy()
+    back = np.stack([oracle.rnea(r, q32[:, b], qd32[:, b], out32[:, b], V0, Vd0, Ft) for b in range(257)], 1)
+    assert rel_err_per_state(back, t32).max() <= TOL[torch.float32]
     nbig = 257 if algo == "aba_scan" else 32                 # beyond the CTA / warp limits
     big = rd.Model.from_robot(synth.random_chain(nbig, 1), synth.GRAVITY_Z)
     big.set_fd_algo(algo)
