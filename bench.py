@@ -76,7 +76,7 @@ class ClockSampler:
                 self.reasons |= int(self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
             except Exception:
                 pass
-            time.sleep(0.01)
+            time.sleep(0.001)
 
     def __enter__(self):
         if self._nv is not None:
