@@ -65,9 +65,15 @@ typedef enum {
   RD_STRAT_WARP_SCAN_EQ13 = 6, /* the paper's operators literally: warp per state, one Eq. (13) semigroup scan
                                   for V and Vdot (Eq. 12) and the Eq. (16) affine backward scan, body frame;
                                   n <= 32 */
-  RD_STRAT_WARP_SCAN_EQ15 = 7  /* the synchronous Eq. (15) scan literally: warp per state, one scan of the
+  RD_STRAT_WARP_SCAN_EQ15 = 7, /* the synchronous Eq. (15) scan literally: warp per state, one scan of the
                                   28x28 operators on (Vdot, Q, V, Fhat, 1) (starred blocks: reading A6),
                                   then the Eq. (16) backward scan; n <= 32; slow (one warp per SM) */
+  RD_STRAT_CHUNK = 8      /* L lanes per state (L = lanes_per_state of rd_model_set_strategy, a power of
+                             two in [2, 32]; 0 = chosen from n), lane j runs the serial recursions over
+                             a chunk of ceil(n/L) consecutive links and the L chunk results are combined
+                             by log2(L)-round shuffle scans of the Eq. (13) semigroup (forward) and of
+                             the Eq. (16) affine wrench maps (backward), at chunk granularity;
+                             revolute (zero pitch) and prismatic joints, any n; screw joints: GENERIC */
 } rd_strategy_t;
 
 /* Forward-dynamics algorithm. */
@@ -117,8 +123,10 @@ int32_t rd_model_n(rd_model_t m);
  * device pointer passed with this model must be memory of that device. */
 int32_t rd_model_device(rd_model_t m);
 
-/* Override the inverse-dynamics strategy (RD_STRAT_AUTO restores the table). */
-rd_status_t rd_model_set_strategy(rd_model_t m, rd_strategy_t s);
+/* Override the inverse-dynamics strategy (RD_STRAT_AUTO restores the table).
+ * lanes_per_state: RD_STRAT_CHUNK only -- 0 (choose from n) or a power of two in
+ * [2, 32]; must be 0 for every other strategy.  RD_E_ARG otherwise. */
+rd_status_t rd_model_set_strategy(rd_model_t m, rd_strategy_t s, int32_t lanes_per_state);
 
 /* Strategy the next rd_inverse_dynamics_* call on `batch` states will use. */
 rd_strategy_t rd_model_resolve_strategy(rd_model_t m, int64_t batch, int32_t fp64);

@@ -25,7 +25,7 @@ __all__ = ["Model", "inverse_dynamics", "forward_dynamics", "inverse_dynamics_ho
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librd.so")
 
 STRATEGIES = {"auto": 0, "thread": 1, "warp_scan": 2, "generic": 3, "reverse": 4, "block_scan": 5,
-              "warp_scan_eq13": 6, "warp_scan_eq15": 7}
+              "warp_scan_eq13": 6, "warp_scan_eq15": 7, "chunk": 8}
 _STRAT_NAMES = {v: k for k, v in STRATEGIES.items()}
 FD_ALGOS = {"aba": 0, "jsiia": 1, "aba_scan": 2, "aba_merged": 3}
 
@@ -65,7 +65,7 @@ def lib():
         L.rd_model_n.restype = i32
         L.rd_model_device.argtypes = [vp]
         L.rd_model_device.restype = i32
-        L.rd_model_set_strategy.argtypes = [vp, ctypes.c_int]
+        L.rd_model_set_strategy.argtypes = [vp, ctypes.c_int, i32]
         L.rd_model_resolve_strategy.argtypes = [vp, i64, i32]
         L.rd_model_resolve_strategy.restype = ctypes.c_int
         L.rd_model_set_boundary.argtypes = [vp, dp, dp, dp]
@@ -131,8 +131,13 @@ class Model:
     def handle(self):
         return self._h
 
-    def set_strategy(self, name: str):
-        _check(lib().rd_model_set_strategy(self._h, STRATEGIES[name]), "rd_model_set_strategy")
+    def set_strategy(self, name: str, lanes_per_state: int = 0):
+        """Inverse-dynamics strategy by name (STRATEGIES); "chunk" takes lanes_per_state
+        (0 = from n), also spelled "chunk:L" (e.g. "chunk:8")."""
+        if name.startswith("chunk:"):
+            name, lanes_per_state = "chunk", int(name.split(":", 1)[1])
+        _check(lib().rd_model_set_strategy(self._h, STRATEGIES[name], int(lanes_per_state)),
+               "rd_model_set_strategy")
 
     def resolve_strategy(self, batch: int, fp64: bool = True) -> str:
         return _STRAT_NAMES[lib().rd_model_resolve_strategy(self._h, int(batch), int(fp64))]

@@ -138,6 +138,7 @@ struct rd_model_s {
   int device = 0;
   bool all_revolute = false;       // every joint revolute with zero pitch
   rd_strategy_t strategy = RD_STRAT_AUTO;
+  int chunk_lanes = 0;             // RD_STRAT_CHUNK: lanes per state (0 = from n)
   rd_fd_algo_t fd_algo = RD_FD_ABA;
   std::vector<rd::LinkConst<double>> L64;
   std::vector<rd::LinkConst<float>> L32;
@@ -488,6 +489,7 @@ rd_strategy_t resolve(rd_model_t m, int64_t batch, bool fp64) {
     case RD_STRAT_BLOCK_SCAN: return m->n <= 512 ? RD_STRAT_BLOCK_SCAN : RD_STRAT_GENERIC;
     case RD_STRAT_WARP_SCAN_EQ13: return warp_ok ? RD_STRAT_WARP_SCAN_EQ13 : RD_STRAT_GENERIC;
     case RD_STRAT_WARP_SCAN_EQ15: return warp_ok ? RD_STRAT_WARP_SCAN_EQ15 : RD_STRAT_GENERIC;
+    case RD_STRAT_CHUNK: return m->dh_ok ? RD_STRAT_CHUNK : RD_STRAT_GENERIC;
     default: break;
   }
   const bool block_ok = !warp_ok && m->n <= 512 && batch <= kBlockScanMaxBatch;
@@ -558,7 +560,7 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     make_state_boundary<T>(m, *usb, true, &sbd);
     pj = &sbj;
     pd = &sbd;
-    if (strat == RD_STRAT_BLOCK_SCAN) strat = m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
+    if (strat == RD_STRAT_BLOCK_SCAN || strat == RD_STRAT_CHUNK) strat = m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
     if (strat == RD_STRAT_WARP_SCAN_EQ13 || strat == RD_STRAT_WARP_SCAN_EQ15)
       return fail(RD_E_UNSUPPORTED, "per-state boundary data: strategies THREAD, WARP_SCAN, GENERIC, REVERSE only");
   }
@@ -588,6 +590,15 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     bool ok = false;
     e = rd::launch_rnea_block<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok);
     if (!ok) strat = RD_STRAT_GENERIC;
+  }
+  if (strat == RD_STRAT_CHUNK) {
+    const int lanes = m->chunk_lanes ? m->chunk_lanes : rd::chunk_default_lanes(m->n);
+    WsScope ws;
+    ws.s = s;
+    st = ws_alloc(m, rd::chunk_ws_elems(m->n, batch, lanes) * sizeof(T), s, &ws.p);
+    if (st != RD_OK) return st;
+    e = rd::launch_rnea_chunk<T>(m->n, lanes, dhc_dev<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches,
+                                 m->has_prism ? m->dPrism : nullptr, reinterpret_cast<T*>(ws.p));
   }
   if (strat == RD_STRAT_REVERSE) {
     e = rd::launch_rnea_rev<T>(m->n, dhc_dev<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches,
@@ -890,10 +901,15 @@ rd_status_t rd_model_destroy(rd_model_t m) {
 int32_t rd_model_n(rd_model_t m) { return m ? m->n : -1; }
 int32_t rd_model_device(rd_model_t m) { return m ? m->device : -1; }
 
-rd_status_t rd_model_set_strategy(rd_model_t m, rd_strategy_t s) {
+rd_status_t rd_model_set_strategy(rd_model_t m, rd_strategy_t s, int32_t lanes_per_state) {
   if (!m) return fail(RD_E_ARG, "null model");
-  if (s < RD_STRAT_AUTO || s > RD_STRAT_WARP_SCAN_EQ15) return fail(RD_E_ARG, "unknown strategy");
+  if (s < RD_STRAT_AUTO || s > RD_STRAT_CHUNK) return fail(RD_E_ARG, "unknown strategy");
+  if (s != RD_STRAT_CHUNK && lanes_per_state != 0) return fail(RD_E_ARG, "lanes_per_state is for RD_STRAT_CHUNK only");
+  if (s == RD_STRAT_CHUNK && lanes_per_state != 0 &&
+      (lanes_per_state < 2 || lanes_per_state > 32 || (lanes_per_state & (lanes_per_state - 1))))
+    return fail(RD_E_ARG, "lanes_per_state must be 0 or a power of two in [2, 32]");
   m->strategy = s;
+  m->chunk_lanes = s == RD_STRAT_CHUNK ? lanes_per_state : 0;
   return RD_OK;
 }
 

@@ -142,6 +142,14 @@ cudaError_t launch_rnea_rev(int n, const LinkDHc<T>* L_dev, const Boundary<T>& b
                             int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
                             cudaStream_t st, int* launches, const unsigned char* prism = nullptr,
                             const StateBoundary<T>* sb = nullptr);
+// CHUNK (rnea_chunk.cu): `lanes` in {2, 4, 8, 16, 32} lanes per state; ws: device
+// workspace of chunk_ws_elems(n, B, lanes) elements.
+template <typename T>
+cudaError_t launch_rnea_chunk(int n, int lanes, const LinkDHc<T>* L_dev, const Boundary<T>& bnd, int64_t B,
+                              const T* q, const T* qd, const T* qdd, T* tau, cudaStream_t st, int* launches,
+                              const unsigned char* prism, T* ws);
+size_t chunk_ws_elems(int n, int64_t B, int lanes);
+int chunk_default_lanes(int n);
 template <typename T>
 cudaError_t launch_aba_dh(int n, const LinkDH<T>* L_dev, const Boundary<T>& bnd,
                           int64_t B, const T* q, const T* qd, const T* tau, T* qdd,

@@ -123,7 +123,7 @@ def test_C5_full_size_sampled(rd):
 
 
 @pytest.mark.parametrize("strategy", ["thread", "generic", "warp_scan", "reverse", "warp_scan_eq13",
-                                      "warp_scan_eq15"])
+                                      "warp_scan_eq15", "chunk:2", "chunk:4", "chunk:8", "chunk:16", "chunk:32"])
 def test_C3_small_all_states(rd, strategy):
     cfg = synth.CONFIGS["C3"]
     q, qd, qdd = synth.states(cfg["seed"], 30, 0, 3000, cfg["ranges"])
@@ -135,8 +135,43 @@ def test_C3_small_all_states(rd, strategy):
 def test_ragged_batches(rd, B):
     r = synth.random_chain(30, 1030)
     q, qd, qdd = synth.states(7, 30, 0, B)
-    for strat in ("auto", "thread", "warp_scan", "generic", "reverse", "warp_scan_eq13", "warp_scan_eq15"):
+    for strat in ("auto", "thread", "warp_scan", "generic", "reverse", "warp_scan_eq13", "warp_scan_eq15",
+                  "chunk:2", "chunk:8", "chunk:32"):
         check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strat)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("n", [1, 2, 7, 30, 31, 64, 100, 200])
+@pytest.mark.parametrize("lanes", [2, 4, 8, 16, 32])
+def test_chunk_strategy_parity(rd, n, lanes, dtype):
+    # RD_STRAT_CHUNK: L lanes per state, chunk scans (rnea_chunk.cu); ragged batch
+    # (last warp partly idle), chunks longer / shorter than n / L, empty tail chunks
+    # (L > n), revolute and prismatic joints
+    for pf, seed in ((0.0, 300 + n), (0.3, 400 + n)):
+        r = synth.random_chain(n, seed, prismatic_fraction=pf)
+        q, qd, qdd = synth.states(24, n, 0, 1037)
+        check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype, strategy=f"chunk:{lanes}")
+
+
+def test_chunk_boundary_and_api(rd):
+    # model-level V_0, Vdot_0, F_{n+1} enter the chunk scans (forward prefix applied to
+    # (V_0, Vdot_0), backward suffix applied to F_{n+1}); lanes_per_state is validated
+    r = synth.random_chain(45, 45, prismatic_fraction=0.2)
+    rng = np.random.default_rng(45)
+    V0, Vd0, Ft = rng.standard_normal((3, 6))
+    model = rd.Model.from_robot(r, (0, 0, 0))
+    model.set_boundary(V0, Vd0, Ft)
+    q, qd, qdd = synth.states(25, 45, 0, 500)
+    ref = np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b], V0, Vd0, Ft) for b in range(500)], 1)
+    for lanes in (0, 2, 4, 8, 16, 32):
+        model.set_strategy("chunk", lanes)
+        tau = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd)).cpu().numpy()
+        assert rel_err_per_state(tau, ref).max() <= 1e-10, lanes
+    for bad in (1, 3, 64, -2):
+        with pytest.raises(rd.RdError):
+            model.set_strategy("chunk", bad)
+    with pytest.raises(rd.RdError):
+        model.set_strategy("thread", 4)
 
 
 def test_auto_strategy_table(rd):
