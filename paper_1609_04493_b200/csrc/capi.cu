@@ -458,51 +458,71 @@ template <typename T> const rd::Boundary<T>& bnd(rd_model_t m);
 template <> const rd::Boundary<double>& bnd<double>(rd_model_t m) { return m->b64; }
 template <> const rd::Boundary<float>& bnd<float>(rd_model_t m) { return m->b32; }
 
-// Strategy table (measured on B200: profiles/r01/
-// crossover.csv, latency.csv, sweep_*.csv).  DH chains (revolute / prismatic):
-//  * n >= 20 (n <= 32) and batch <= 2048 -> WARP_SCAN: one warp per state, lane =
-//    link, log-depth shuffle scans; the latency regime (paper P:505/P:524), e.g.
-//    n = 30, B = 2048: 26 us vs 29 us (REVERSE) and 39 us (THREAD);
-//  * batch above the thread crossover (fp64 32768, fp32 49152) and the on-chip
-//    stash fits (n <= 30 fp64 / 32 fp32) -> THREAD: e.g. n = 30, B = 1M: 6.3x
-//    WARP_SCAN; below it one tile per SM is latency-bound (2n serial link steps),
-//    and the 16-warp stash-free REVERSE wins (n = 30, B = 16384: 30 vs 39 us);
-//  * n > 32 and batch <= 1024 -> BLOCK_SCAN: one CTA per state (NEXT-3), e.g.
-//    n = 512, B = 1: 29 us vs 213 us (REVERSE), 650 us (GENERIC);
-//  * otherwise REVERSE.
+// Strategy table, measured on B200 as device time
+// per call (CUDA-graph replay; profiles/r02/auto_grid_f64.csv, auto_grid_f32.csv).
+// DH chains (revolute / prismatic joints):
+//  * n <= 32: WARP_SCAN (warp per state, lane = link; the latency regime of the
+//    paper) for batch <= 1536 (fp64: n >= 7; fp32: n >= 20), e.g. n = 30,
+//    B = 1000: 6.1 us vs 9.7 (CHUNK 16) / 10.4 (BLOCK_SCAN); up to 3072 for n >= 24
+//    (n = 30, B = 2048: 10.4 vs 11.3 us CHUNK 8); CHUNK with 8 / 4 lanes for
+//    16 <= n <= 32 at batches up to 3072 / 6144 (n = 30, B = 4096: 13.2 vs
+//    14.0 us REVERSE); THREAD above the thread crossover (fp64 32768, fp32 49152;
+//    n = 30, B = 65536: 38 vs 43 us) when the on-chip stash fits (n <= 30 fp64 /
+//    32 fp32); REVERSE in between;
+//  * n > 32: BLOCK_SCAN (CTA per state) for batch <= 512 (<= 1024 fp32 n < 100);
+//    CHUNK with 16 (32 for n >= 150) lanes up to 1536, 8 lanes up to 3072, 4 (8 for
+//    n >= 150) lanes up to 6144 (n = 100, B = 1000 / 2048 / 4096: 16 / 19 / 27 us vs
+//    BLOCK_SCAN 33 / REVERSE 40 us); REVERSE above (and for n > 300 from 3072 on).
 // Screw joints (no DH form): WARP_SCAN for n <= 32 and batch <= 4096, BLOCK_SCAN
 // for longer chains and batch <= 1024, else GENERIC.
 constexpr int64_t kWarpScanMaxBatch = 4096;     // joint-frame chains
-constexpr int64_t kWarpScanMaxBatchDH = 2048;   // DH chains, n >= kWarpScanMinN
-constexpr int kWarpScanMinN = 20;
 constexpr int64_t kBlockScanMaxBatch = 1024;
 constexpr int64_t kThreadMinBatch64 = 32768, kThreadMinBatch32 = 49152;
 
-rd_strategy_t resolve(rd_model_t m, int64_t batch, bool fp64) {
-  const bool thread_ok = m->dh_ok && rd::thread_kernel_has_n(m->n, fp64);
-  const bool warp_ok = m->n <= 32;
+struct Plan {
+  rd_strategy_t s;
+  int lanes;        // CHUNK: lanes per state
+};
+
+Plan resolve_plan(rd_model_t m, int64_t batch, bool fp64) {
+  const int n = m->n;
+  const bool thread_ok = m->dh_ok && rd::thread_kernel_has_n(n, fp64);
+  const bool warp_ok = n <= 32;
   switch (m->strategy) {
-    case RD_STRAT_GENERIC: return RD_STRAT_GENERIC;
-    case RD_STRAT_THREAD: return thread_ok ? RD_STRAT_THREAD : (m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC);
-    case RD_STRAT_WARP_SCAN: return warp_ok ? RD_STRAT_WARP_SCAN : RD_STRAT_GENERIC;
-    case RD_STRAT_REVERSE: return m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
-    case RD_STRAT_BLOCK_SCAN: return m->n <= 512 ? RD_STRAT_BLOCK_SCAN : RD_STRAT_GENERIC;
-    case RD_STRAT_WARP_SCAN_EQ13: return warp_ok ? RD_STRAT_WARP_SCAN_EQ13 : RD_STRAT_GENERIC;
-    case RD_STRAT_WARP_SCAN_EQ15: return warp_ok ? RD_STRAT_WARP_SCAN_EQ15 : RD_STRAT_GENERIC;
-    case RD_STRAT_CHUNK: return m->dh_ok ? RD_STRAT_CHUNK : RD_STRAT_GENERIC;
+    case RD_STRAT_GENERIC: return {RD_STRAT_GENERIC, 0};
+    case RD_STRAT_THREAD: return {thread_ok ? RD_STRAT_THREAD : (m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC), 0};
+    case RD_STRAT_WARP_SCAN: return {warp_ok ? RD_STRAT_WARP_SCAN : RD_STRAT_GENERIC, 0};
+    case RD_STRAT_REVERSE: return {m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC, 0};
+    case RD_STRAT_BLOCK_SCAN: return {n <= 512 ? RD_STRAT_BLOCK_SCAN : RD_STRAT_GENERIC, 0};
+    case RD_STRAT_WARP_SCAN_EQ13: return {warp_ok ? RD_STRAT_WARP_SCAN_EQ13 : RD_STRAT_GENERIC, 0};
+    case RD_STRAT_WARP_SCAN_EQ15: return {warp_ok ? RD_STRAT_WARP_SCAN_EQ15 : RD_STRAT_GENERIC, 0};
+    case RD_STRAT_CHUNK:
+      if (!m->dh_ok) return {RD_STRAT_GENERIC, 0};
+      return {RD_STRAT_CHUNK, m->chunk_lanes ? m->chunk_lanes : rd::chunk_default_lanes(n)};
     default: break;
   }
-  const bool block_ok = !warp_ok && m->n <= 512 && batch <= kBlockScanMaxBatch;
   if (m->dh_ok) {
-    if (warp_ok && m->n >= kWarpScanMinN && batch <= kWarpScanMaxBatchDH) return RD_STRAT_WARP_SCAN;
-    if (thread_ok && batch > (fp64 ? kThreadMinBatch64 : kThreadMinBatch32)) return RD_STRAT_THREAD;
-    if (block_ok) return RD_STRAT_BLOCK_SCAN;
-    return RD_STRAT_REVERSE;
+    if (warp_ok) {
+      if (batch <= 1536 && n >= (fp64 ? 7 : 20)) return {RD_STRAT_WARP_SCAN, 0};
+      if (batch <= 3072 && n >= 24) return {RD_STRAT_WARP_SCAN, 0};
+      if (n >= 16 && batch <= 3072) return {RD_STRAT_CHUNK, 8};
+      if (n >= 24 && batch <= 6144) return {RD_STRAT_CHUNK, 4};
+      if (thread_ok && batch > (fp64 ? kThreadMinBatch64 : kThreadMinBatch32)) return {RD_STRAT_THREAD, 0};
+      return {RD_STRAT_REVERSE, 0};
+    }
+    const int64_t block_max = (!fp64 && n < 100) ? 1024 : 512;
+    if (n <= 512 && batch <= block_max) return {RD_STRAT_BLOCK_SCAN, 0};
+    if (batch <= 1536) return {RD_STRAT_CHUNK, n >= 150 ? 32 : 16};
+    if (batch <= 3072) return {RD_STRAT_CHUNK, 8};
+    if (batch <= 6144 && n <= 300) return {RD_STRAT_CHUNK, n >= 150 ? 8 : 4};
+    return {RD_STRAT_REVERSE, 0};
   }
-  if (warp_ok && batch <= kWarpScanMaxBatch) return RD_STRAT_WARP_SCAN;
-  if (block_ok) return RD_STRAT_BLOCK_SCAN;
-  return RD_STRAT_GENERIC;
+  if (warp_ok && batch <= kWarpScanMaxBatch) return {RD_STRAT_WARP_SCAN, 0};
+  if (!warp_ok && n <= 512 && batch <= kBlockScanMaxBatch) return {RD_STRAT_BLOCK_SCAN, 0};
+  return {RD_STRAT_GENERIC, 0};
 }
+
+rd_strategy_t resolve(rd_model_t m, int64_t batch, bool fp64) { return resolve_plan(m, batch, fp64).s; }
 
 // Per-state boundary arrays (NEXT-4): validated device arrays [6][batch] -> the
 // kernel-side StateBoundary for joint-frame (jf) and DH kernels.
@@ -544,12 +564,13 @@ void make_state_boundary(rd_model_t m, const UserStateBoundary& u, bool dh, rd::
 template <typename T>
 rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* qd, const T* qdd, T* tau,
                              void* stream, const UserStateBoundary* usb = nullptr,
-                             rd_strategy_t force = RD_STRAT_AUTO) {
+                             Plan force = Plan{RD_STRAT_AUTO, 0}) {
   g_launches = 0;
   rd_status_t st = check_io<T>(m, batch, q, qd, qdd, tau, true);
   if (st != RD_OK || batch == 0) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  rd_strategy_t strat = force != RD_STRAT_AUTO ? force : resolve(m, batch, sizeof(T) == 8);
+  Plan plan = force.s != RD_STRAT_AUTO ? force : resolve_plan(m, batch, sizeof(T) == 8);
+  rd_strategy_t strat = plan.s;
   rd::StateBoundary<T> sbj, sbd;                 // joint-frame / DH variants
   const rd::StateBoundary<T>* pj = nullptr;
   const rd::StateBoundary<T>* pd = nullptr;
@@ -592,7 +613,7 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     if (!ok) strat = RD_STRAT_GENERIC;
   }
   if (strat == RD_STRAT_CHUNK) {
-    const int lanes = m->chunk_lanes ? m->chunk_lanes : rd::chunk_default_lanes(m->n);
+    const int lanes = plan.lanes ? plan.lanes : rd::chunk_default_lanes(m->n);
     WsScope ws;
     ws.s = s;
     st = ws_alloc(m, rd::chunk_ws_elems(m->n, batch, lanes) * sizeof(T), s, &ws.p);
@@ -1011,7 +1032,7 @@ rd_status_t host_pipeline(rd_model_t m, int64_t batch, const double* q, const do
   if (dev != m->device) return fail(RD_E_ARG, "current CUDA device differs from the model's device");
   std::lock_guard<std::mutex> lk(m->host_mu);
   const int n = m->n;
-  const rd_strategy_t strat = FD ? RD_STRAT_AUTO : resolve(m, batch, true);
+  const Plan plan = FD ? Plan{RD_STRAT_AUTO, 0} : resolve_plan(m, batch, true);
   const int64_t chunk = std::min<int64_t>(batch, std::max<int64_t>(4096, chunk_bytes / (8ll * n)));
   const size_t set_bytes = (size_t)4 * n * chunk * sizeof(double);
   if (m->hbuf_bytes < set_bytes) {
@@ -1049,7 +1070,7 @@ rd_status_t host_pipeline(rd_model_t m, int64_t batch, const double* q, const do
     if (e == cudaSuccess) e = cudaMemcpy2DAsync(d3, dp, third + b0, hp, dp, n, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) { result = cuda_fail(e, "host path H2D"); break; }
     st = FD ? forward_dynamics<double>(m, bc, dq, dqd, d3, dout, s)
-            : inverse_dynamics<double>(m, bc, dq, dqd, d3, dout, s, nullptr, strat);
+            : inverse_dynamics<double>(m, bc, dq, dqd, d3, dout, s, nullptr, plan);
     launches += g_launches;
     if (st != RD_OK) { result = st; break; }
     e = cudaMemcpy2DAsync(out + b0, hp, dout, dp, dp, n, cudaMemcpyDeviceToHost, s);

@@ -182,10 +182,13 @@ def test_auto_strategy_table(rd):
     screw = synth.random_chain(12, 77)
     screw["S"][0, :3] += 0.2 * screw["S"][0, 3:]
     sc = rd.Model.from_robot(screw, synth.GRAVITY_Z)
-    for model, B, fp64, want in [(dh30, 1000, True, "warp_scan"), (dh30, 16384, True, "reverse"),
+    for model, B, fp64, want in [(dh30, 1000, True, "warp_scan"), (dh30, 2048, True, "warp_scan"),
+                                 (dh30, 4096, True, "chunk"), (dh30, 16384, True, "reverse"),
                                  (dh30, 1_000_000, True, "thread"), (dh30, 40000, False, "reverse"),
-                                 (dh30, 60000, False, "thread"), (dh10, 1000, True, "reverse"),
-                                 (dh10, 100_000, True, "thread"), (dh100, 64, True, "block_scan"),
+                                 (dh30, 60000, False, "thread"), (dh10, 1000, True, "warp_scan"),
+                                 (dh10, 1000, False, "reverse"), (dh10, 100_000, True, "thread"),
+                                 (dh100, 64, True, "block_scan"), (dh100, 1000, True, "chunk"),
+                                 (dh100, 4096, True, "chunk"), (dh100, 16384, True, "reverse"),
                                  (dh100, 100_000, True, "reverse"), (sc, 1000, True, "warp_scan"),
                                  (sc, 100_000, True, "generic")]:
         assert model.resolve_strategy(B, fp64) == want, (model.n, B, fp64, want)
@@ -386,7 +389,7 @@ def test_deterministic_and_strategy_consistent(rd):
     cfg = synth.CONFIGS["C3"]
     q, qd, qdd = synth.states(cfg["seed"], 30, 0, 20000)
     model = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
-    for strat in ("thread", "warp_scan", "generic", "reverse"):
+    for strat in ("thread", "warp_scan", "generic", "reverse", "chunk:4"):
         # with a FIXED strategy, results are bit-identical across repeats and across sharding
         # (AUTO picks the strategy from the per-call batch size)
         model.set_strategy(strat)

@@ -29,8 +29,7 @@ if a.batch:
     cfg.update(batch=a.batch)
 n = cfg["n"]
 dt = torch.float64 if a.dtype == "f64" else torch.float32
-q, qd, qdd = synth.states(cfg["seed"], n, 0, cfg["batch"], cfg["ranges"])
-tq, tqd, tqdd = (torch.from_numpy(x).to("cuda", dt) for x in (q, qd, qdd))
+tq, tqd, tqdd = synth.states_device(cfg["seed"], n, 0, cfg["batch"], cfg["ranges"], dtype=dt)
 m = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
 m.set_strategy(a.strategy)
 m.set_fd_algo(a.fd_algo)

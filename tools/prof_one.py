@@ -16,10 +16,11 @@ a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 n = cfg["n"]; B = a.batch or cfg["batch"]
 dt = torch.float64 if a.dtype == "f64" else torch.float32
-q, qd, qdd = synth.states(cfg["seed"], n, 0, B, cfg["ranges"])
-tq, tqd, tqdd = (torch.from_numpy(x).to("cuda", dt) for x in (q, qd, qdd))
+tq, tqd, tqdd = synth.states_device(cfg["seed"], n, 0, B, cfg["ranges"], dtype=dt)
 m = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
 m.set_strategy(a.strategy)
+if a.fd:                                    # consistent torques for the FD run
+    tqdd = rd.inverse_dynamics(m, tq, tqd, tqdd).clone()
 out = torch.empty_like(tq)
 for _ in range(a.reps):
     if a.fd:
