@@ -18,8 +18,8 @@ for dt in (torch.float64, torch.float32):
             q, qd, qdd = (torch.from_numpy(x).to("cuda", dt) for x in synth.states(1, n, 0, B))
             skip = os.environ.get("SKIP_STRATS", "").split(",")
             for strat in ("thread", "warp_scan", "generic", "reverse", "block_scan", "warp_scan_eq13",
-                          "warp_scan_eq15"):
-                if strat in skip:
+                          "warp_scan_eq15", "chunk:2", "chunk:4", "chunk:8", "chunk:32"):
+                if strat.split(":")[0] in skip:
                     continue
                 model.set_strategy(strat)
                 rd.inverse_dynamics(model, q, qd, qdd)
