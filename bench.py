@@ -157,13 +157,15 @@ def cpu_baseline_fd(robot, g, cfg, n, seconds=10.0):
 
 
 def load_traffic(cfg_name: str, dtype: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
+    capture (profiles/ncu_traffic.json, tools/ncu_traffic.py) and the capture it came from."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(f"{cfg_name}_{dtype}")
+        return d.get(f"{cfg_name}_{dtype}"), d.get(f"{cfg_name}_{dtype}_source")
     except Exception:
-        return None
+        return None, None
 
 
 def run_reference(args):
@@ -393,7 +395,7 @@ def main():
     flops = (lean_flops_fd(n) if fd else lean_flops_id(n)) * per_gpu
     achieved = flops / (avg_kernel_ms / 1e3) / 1e12
     peak = PEAK_F64_TFLOPS if args.dtype == "f64" else PEAK_F32_TFLOPS
-    traffic = load_traffic(args.config, args.dtype)
+    traffic, traffic_src = load_traffic(args.config, args.dtype)
     strat = model.resolve_strategy(per_gpu, args.dtype == "f64") if not fd else "aba_thread"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -408,13 +410,15 @@ def main():
                    "strategy": strat, "robot_seed": 1000 + n if cfg["robot"] == "random" else cfg["robot"],
                    "state_seed": cfg["seed"], "l2": l2_note},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes": (32 if args.dtype == "f64" else 16) * n * per_gpu,
                      "flops_per_eval": lean_flops_fd(n) if fd else lean_flops_id(n),
                      "peak_basis": "148 SM x 64 DFMA/clk x 2 x 1.965 GHz (guide unit counts; measured DFMA "
                                    "microbench 34.0 TF/s, profiles/r01/peaks_alu.jsonl)"
                                    + ("; fp32 = 2x" if args.dtype == "f32" else ""),
                      "kernel_ms": avg_kernel_ms,
-                     "hbm_gbs": 32 * n * per_gpu / (avg_kernel_ms / 1e3) / 1e9 * (0.5 if args.dtype == "f32" else 1)},
+                     "algorithmic_hbm_gbs": 32 * n * per_gpu / (avg_kernel_ms / 1e3) / 1e9
+                                            * (0.5 if args.dtype == "f32" else 1)},
         "clocks": clock.summary(),
         "gpu_launches": launches,
         "e2e": e2e,

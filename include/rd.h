@@ -53,9 +53,11 @@ typedef enum {
 /* In-robot parallelisation strategy of the inverse-dynamics kernel (north_star (2)). */
 typedef enum {
   RD_STRAT_AUTO = 0,      /* chosen per (n, dtype, batch) from the measured table */
-  RD_STRAT_THREAD = 1,    /* one thread per state, serial recursion, per-link stash on chip (TMEM + shared
-                             memory); revolute (zero pitch) and prismatic joints, n <= 30 fp64 / 32 fp32;
-                             otherwise falls back to REVERSE (screw joints: GENERIC) */
+  RD_STRAT_THREAD = 1,    /* one thread per state, serial recursion; revolute (zero pitch) and prismatic
+                             joints.  Short chains (fp64 n <= 8, or n <= 12 up to 300000 states; fp32
+                             n <= 32 except 25, 26) keep the whole per-link stash in registers (fully
+                             unrolled register kernel); longer ones stash on chip (TMEM + shared memory),
+                             n <= 30 fp64 / 32 fp32; otherwise falls back to REVERSE (screw: GENERIC) */
   RD_STRAT_WARP_SCAN = 2, /* one warp per state, lane = link, Kogge-Stone shuffle scans */
   RD_STRAT_GENERIC = 3,   /* one thread per state, any n, any joints, stash in a global workspace */
   RD_STRAT_REVERSE = 4,   /* one thread per state, any n (revolute / prismatic joints; screw: GENERIC),

@@ -25,20 +25,36 @@
 #include "rd_internal.h"
 #include "rd_math.cuh"
 #include "rd_aba.cuh"
+#include "rd_async.cuh"
 
 namespace rd {
 
-// Workspace read-ahead of sweep 3 (links), input prefetch distances / unroll
-// factors of the DH kernel's sweeps 1 and 3 (short iterations; see
-// rnea_thread.cu StepCfg for why unroll ~ distance), and the DH kernel's minimum
-// resident CTAs of kAbaThreads per SM (register cap).  Measured on B200, C4:
-// sweep-3 distance / unroll 2 / 2 0.4578 ms vs 1 / 2 0.4604 ms.
-constexpr int kWsPD = 2;
-constexpr int kAbaMinBlocks = 3;
-constexpr int kS1PD = 4, kS1U = 4, kS3PD = 2, kS3U = 2;
-constexpr int kAbaPerLink = 7;   // Ubar = U/D (6), ubar = u/D
+constexpr int kAbaPerLink = 7;   // joint-frame kernel: Ubar = U/D (6), ubar = u/D, SoA [link][7][slot]
 constexpr int kAbaThreads = 128;
-int aba_ws_per_link() { return kAbaPerLink; }
+// The DH kernel's minimum resident CTAs of kAbaThreads per SM (register cap) and the
+// depth of its shared-memory ring (stages; sweeps 1 and 3 read kRing - 1 links ahead).
+// Measured on B200 (A/B, profiles/r02/ab_aba_ring.txt): fp64 C4 0.442 ms (register
+// prefetch, 3 CTAs) -> 0.426 ms (ring 4, 4 CTAs; ring 6 at 3 CTAs 0.437); fp32 C4
+// 0.311 -> 0.294 ms with ring 6-7 (ring 4: 0.325) -- fp32 wants depth, fp64 warps.
+template <typename T>
+struct AbaCfg {
+  static constexpr int kMinBlocks = 4;
+  static constexpr int kRing = sizeof(T) == 8 ? 4 : 7;
+};
+int aba_ws_per_link() { return 8; }   // max(kAbaPerLink, AbaWs<double, true>::kV)
+
+// DH kernel workspace: per (link, slot) one contiguous record of kV scalars,
+// [link][slot][kV], written by sweep 2 as kChunks 16-byte stores and read back by
+// sweep 3 as kChunks 16-byte cp.async copies.  Revolute fp64: (Ubar_0..4, ubar)
+// = 48 B (Ubar_5 = 1 is not stored); prismatic fp64: (Ubar_0..5, ubar, pad);
+// fp32: 8 scalars (padded to 32 B).
+template <typename T, bool PR>
+struct AbaWs {
+  static constexpr int kV = (sizeof(T) == 8) ? (PR ? 8 : 6) : 8;
+  static constexpr int kChunks = kV * (int)sizeof(T) / 16;
+  // one ring stage: kChunks x [thread] 16-byte vectors, then q [thread], qd [thread]
+  static constexpr int kStageBytes = kAbaThreads * (kChunks * 16 + 2 * (int)sizeof(T));
+};
 
 template <typename T, bool SB>
 __global__ void __launch_bounds__(kAbaThreads)
@@ -195,6 +211,12 @@ aba_kernel(int n, const LinkConst<T>* __restrict__ L, const Boundary<T> bnd, int
 // 22-flop Ad maps.  Revolute S = (0, e_z): U = Jhat[:, 5], D = U[5],
 // u = tau - phat[5]; prismatic (PR instantiation, per-link flag) S = (e_z, 0):
 // U = Jhat[:, 2], D = U[2], u = tau - phat[2], d = d0 + q.
+// Shared memory of the DH kernel: constants, prismatic flags, then the ring (16-byte aligned).
+template <typename T>
+__host__ __device__ constexpr size_t aba_ring_offset(int n, bool PR) {
+  return ((size_t)n * sizeof(LinkDH<T>) + (PR ? (size_t)n : 0) + 15) / 16 * 16;
+}
+
 template <typename T, int MB, bool PR, bool SB>
 __global__ void __launch_bounds__(kAbaThreads, MB)
 aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, int64_t B,
@@ -205,6 +227,8 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LinkDH<T>* L = reinterpret_cast<LinkDH<T>*>(smem_raw);
   unsigned char* PRs = smem_raw + (size_t)n * sizeof(LinkDH<T>);   // prismatic flags (PR only)
+  // the ring of sweeps 1 and 3 (aba_ring_offset): AbaCfg<T>::kRing stages of AbaWs::kStageBytes
+  unsigned char* ring = smem_raw + aba_ring_offset<T>(n, PR);
   for (int i = threadIdx.x; i < n * (int)(sizeof(LinkDH<T>) / sizeof(T)); i += blockDim.x)
     reinterpret_cast<T*>(L)[i] = reinterpret_cast<const T*>(Lg)[i];
   if (PR)
@@ -223,23 +247,32 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
     if constexpr (SB) {                              // per-state V_0 (NEXT-4)
       if (sb.V0) sb_vec(sb.V0, sb.A0, B, b, V);
     }
-    // sweep 1: V_n only; inputs kS1PD links ahead
-    {
-      T aq[kS1PD], aqd[kS1PD];
-#pragma unroll
-      for (int j = 0; j < kS1PD; ++j) {
-        const int64_t o = (int64_t)min(j, n - 1) * B;
-        aq[j] = __ldg(pq + o); aqd[j] = __ldg(pqd + o);
+    // sweep 1: V_n only.  q, qd stream through the shared-memory ring AbaCfg<T>::kRing - 1
+    // links ahead (cp.async; a sweep-1 step is ~45 FP64 instructions, far shorter
+    // than a DRAM round trip, and the ring holds no registers)
+    const int tid = threadIdx.x;
+    using WS = AbaWs<T, PR>;
+    auto ring_q = [&](int st) { return reinterpret_cast<T*>(ring + st * WS::kStageBytes + WS::kChunks * 16 * kAbaThreads) + tid; };
+    auto ring_ws = [&](int st, int j) {
+      return reinterpret_cast<T*>(ring + st * WS::kStageBytes + (j * kAbaThreads + tid) * 16);
+    };
+    auto issue_in = [&](int j, int st) {          // q, qd of link j into stage st (one group per link)
+      if (j < n) {
+        cp_async_elem(ring_q(st), pq + (int64_t)j * B);
+        cp_async_elem(ring_q(st) + kAbaThreads, pqd + (int64_t)j * B);
       }
-#pragma unroll (kS1U)
-      for (int i = 0; i < n; ++i) {
-        const T cq = aq[0], cqd = aqd[0];
+    };
+    {
 #pragma unroll
-        for (int j = 0; j + 1 < kS1PD; ++j) { aq[j] = aq[j + 1]; aqd[j] = aqd[j + 1]; }
-        {
-          const int64_t o = (int64_t)min(i + kS1PD, n - 1) * B;
-          aq[kS1PD - 1] = __ldg(pq + o); aqd[kS1PD - 1] = __ldg(pqd + o);
-        }
+      for (int j = 0; j < AbaCfg<T>::kRing - 1; ++j) { issue_in(j, j); cp_async_commit(); }
+      int st = 0;
+      for (int i = 0; i < n; ++i) {
+        cp_async_wait<AbaCfg<T>::kRing - 2>();            // link i's group has landed
+        const T cq = *ring_q(st), cqd = ring_q(st)[kAbaThreads];
+        const int sp = (st == 0) ? AbaCfg<T>::kRing - 1 : st - 1;   // consumed one step ago
+        issue_in(i + AbaCfg<T>::kRing - 1, sp);
+        cp_async_commit();
+        st = (st == AbaCfg<T>::kRing - 1) ? 0 : st + 1;
         const LinkDH<T>& C = L[i];
         T Vn[6];
         if constexpr (PR) {
@@ -304,11 +337,22 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
       const T invD = (D > (T)0) ? (T)1 / D : (T)NAN;
       if (!(D > (T)0) && fail == 0) fail = i + 1;
       const T ub = (ct - ((PR && pz) ? ph[2] : ph[5])) * invD;
-      T* w = ws + (int64_t)i * kAbaPerLink * slots + slot;
+      {                                                   // one record [link][slot][kV], 16-byte stores
+        T rec[WS::kV];
 #pragma unroll
-      for (int k = 0; k < 6; ++k)
-        if (PR || k != 5) w[k * slots] = U[k] * invD;   // revolute: Ubar_5 = U_5 / D = 1, not stored
-      w[6 * slots] = ub;
+        for (int k = 0; k < 5; ++k) rec[k] = U[k] * invD;
+        if constexpr (WS::kV == 6) {
+          rec[5] = ub;                                    // revolute fp64: Ubar_5 = U_5 / D = 1, not stored
+        } else {
+          rec[5] = U[5] * invD;
+          rec[6] = ub;
+          rec[7] = T(0);
+        }
+        T* w = ws + ((int64_t)i * slots + slot) * WS::kV;
+#pragma unroll
+        for (int j = 0; j < WS::kChunks; ++j)
+          *reinterpret_cast<uint4*>(w + j * (16 / sizeof(T))) = *reinterpret_cast<const uint4*>(rec + j * (16 / sizeof(T)));
+      }
       if (i > 0) {
         if constexpr (PR) sym6_rank1_sub(K, U, invD);     // Jhat^a
         else sym6_rank1_sub_rev(K, U, invD);
@@ -347,57 +391,50 @@ aba_dh_kernel(int n, const LinkDH<T>* __restrict__ Lg, const Boundary<T> bnd, in
       if (sb.Vd0) sb_vec(sb.Vd0, sb.A0, B, b, a);
     }
     {
-      T bq[kS3PD], bqd[kS3PD];
+      // (Ubar, ubar) records, q and qd of link i + AbaCfg<T>::kRing - 1 are copied into the
+      // ring while link i computes: the workspace comes back from DRAM (560 MB at
+      // C4 does not fit in L2) and a sweep-3 step is short
+      auto issue_all = [&](int j, int st) {
+        if (j < n) {
+          const T* w = ws + ((int64_t)j * slots + slot) * WS::kV;
 #pragma unroll
-      for (int j = 0; j < kS3PD; ++j) {
-        const int64_t o = (int64_t)min(j, n - 1) * B;
-        bq[j] = __ldg(pq + o); bqd[j] = __ldg(pqd + o);
-      }
-      // (Ubar, ubar) of links i .. i+kWsPD-1 in flight: the workspace reads come from
-      // DRAM (it does not fit in L2) and a sweep-3 step is short
-      constexpr int PD = kWsPD;
-      T cU[PD][7];
-#pragma unroll
-      for (int j = 0; j < PD; ++j)
-#pragma unroll
-        for (int k = 0; k < 7; ++k)
-          cU[j][k] = (PR || k != 5) ? ws[((int64_t)min(j, n - 1) * kAbaPerLink + k) * slots + slot] : T(1);
-#pragma unroll (kS3U)
-      for (int i = 0; i < n; ++i) {
-        const T cq3 = bq[0], cqd3 = bqd[0];
-#pragma unroll
-        for (int j = 0; j + 1 < kS3PD; ++j) { bq[j] = bq[j + 1]; bqd[j] = bqd[j + 1]; }
-        {
-          const int64_t o = (int64_t)min(i + kS3PD, n - 1) * B;
-          bq[kS3PD - 1] = __ldg(pq + o); bqd[kS3PD - 1] = __ldg(pqd + o);
+          for (int c = 0; c < WS::kChunks; ++c) cp_async_16(ring_ws(st, c), w + c * (16 / sizeof(T)));
+          issue_in(j, st);
         }
-        const LinkDH<T>& C = L[i];
+      };
+#pragma unroll
+      for (int j = 0; j < AbaCfg<T>::kRing - 1; ++j) { issue_all(j, j); cp_async_commit(); }
+      int st = 0;
+      for (int i = 0; i < n; ++i) {
+        cp_async_wait<AbaCfg<T>::kRing - 2>();
+        T rec[WS::kV];
+#pragma unroll
+        for (int c = 0; c < WS::kChunks; ++c)
+          *reinterpret_cast<uint4*>(rec + c * (16 / sizeof(T))) = *reinterpret_cast<const uint4*>(ring_ws(st, c));
+        const T cq3 = *ring_q(st), cqd3 = ring_q(st)[kAbaThreads];
+        const int sp = (st == 0) ? AbaCfg<T>::kRing - 1 : st - 1;
+        issue_all(i + AbaCfg<T>::kRing - 1, sp);
+        cp_async_commit();
+        st = (st == AbaCfg<T>::kRing - 1) ? 0 : st + 1;
         T Ub[6];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) Ub[k] = cU[0][k];
-        const T ub = cU[0][6];
-#pragma unroll
-        for (int j = 0; j + 1 < PD; ++j)
-#pragma unroll
-          for (int k = 0; k < 7; ++k) cU[j][k] = cU[j + 1][k];
-        {
-          const T* wn = ws + (int64_t)min(i + PD, n - 1) * kAbaPerLink * slots + slot;
-#pragma unroll
-          for (int k = 0; k < 7; ++k) cU[PD - 1][k] = (PR || k != 5) ? wn[k * slots] : T(1);
-        }
+        for (int k = 0; k < 5; ++k) Ub[k] = rec[k];
+        Ub[5] = (WS::kV == 6) ? T(1) : rec[5];
+        const T ub = (WS::kV == 6) ? rec[5] : rec[6];
+        const LinkDH<T>& C = L[i];
         const bool pz = PR && PRs[i];
         const T qdi = cqd3;
         T Vn[6], an[6];
         if constexpr (PR) {
           T s, c, dl;
           dh_link<PR>(C, pz, cq3, &s, &c, &dl);
-          const T sr = pz ? T(0) : qdi, sp = pz ? qdi : T(0);
+          const T sr = pz ? T(0) : qdi, sp2 = pz ? qdi : T(0);
           dh_ad_finv(C.ca, C.sa, C.a, dl, s, c, V, Vn);
           Vn[5] += sr;
-          Vn[2] += sp;
+          Vn[2] += sp2;
           dh_ad_finv(C.ca, C.sa, C.a, dl, s, c, a, an);
-          an[0] = fma(sr, Vn[1], fma(sp, Vn[4], an[0]));
-          an[1] = fma(-sr, Vn[0], fma(-sp, Vn[3], an[1]));
+          an[0] = fma(sr, Vn[1], fma(sp2, Vn[4], an[0]));
+          an[1] = fma(-sr, Vn[0], fma(-sp2, Vn[3], an[1]));
           an[3] = fma(sr, Vn[4], an[3]);
           an[4] = fma(-sr, Vn[3], an[4]);
         } else {
@@ -431,13 +468,13 @@ static cudaError_t launch_aba_dh_pr(int n, const LinkDH<T>* L_dev, const Boundar
                                     cudaStream_t st, int32_t* status, const unsigned char* prism,
                                     const typename SBArg<T, SB>::type& sb) {
   const int64_t grid = (ws_slots + kAbaThreads - 1) / kAbaThreads;
-  const size_t smem = (size_t)n * sizeof(LinkDH<T>) + (PR ? (size_t)n : 0);
+  const size_t smem = aba_ring_offset<T>(n, PR) + (size_t)AbaCfg<T>::kRing * AbaWs<T, PR>::kStageBytes;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(aba_dh_kernel<T, kAbaMinBlocks, PR, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(aba_dh_kernel<T, AbaCfg<T>::kMinBlocks, PR, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  aba_dh_kernel<T, kAbaMinBlocks, PR, SB><<<(unsigned)grid, kAbaThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws,
+  aba_dh_kernel<T, AbaCfg<T>::kMinBlocks, PR, SB><<<(unsigned)grid, kAbaThreads, smem, st>>>(n, L_dev, bnd, B, q, qd, tau, qdd, ws,
                                                                           ws_slots, status, prism, sb);
   return cudaGetLastError();
 }

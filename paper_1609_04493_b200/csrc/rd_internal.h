@@ -106,6 +106,13 @@ cudaError_t launch_rnea_thread(int n, const LinkDHc<T>* L_host, const Boundary<T
                                int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
                                cudaStream_t st, int* launches, bool* supported, uint32_t prism_mask = 0,
                                const StateBoundary<T>* sb = nullptr);
+// Short chains (n <= 12 fp64 / 16 fp32, no per-state boundary): the register-resident, fully
+// unrolled THREAD kernel (rnea_small.cu); launch_rnea_thread dispatches to it.
+bool small_kernel_has_n(int n, bool fp64, int64_t batch);
+template <typename T>
+cudaError_t launch_rnea_small(int n, const LinkDHc<T>* L_host, const Boundary<T>& bnd, int64_t B, const T* q,
+                              const T* qd, const T* qdd, T* tau, cudaStream_t st, int* launches,
+                              uint32_t prism_mask, const StateBoundary<T>* sb = nullptr);
 template <typename T>
 cudaError_t launch_rnea_generic(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd,
                                 int64_t B, const T* q, const T* qd, const T* qdd, T* tau,

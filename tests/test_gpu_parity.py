@@ -178,19 +178,23 @@ def test_auto_strategy_table(rd):
     # the measured AUTO table (csrc/capi.cu resolve())
     dh30 = rd.Model.from_robot(synth.random_chain(30, 1030), synth.GRAVITY_Z)
     dh10 = rd.Model.from_robot(synth.random_chain(10, 1010), synth.GRAVITY_Z)
+    dh7 = rd.Model.from_robot(synth.random_chain(7, 1007), synth.GRAVITY_Z)
     dh100 = rd.Model.from_robot(synth.random_chain(100, 1100), synth.GRAVITY_Z)
     screw = synth.random_chain(12, 77)
     screw["S"][0, :3] += 0.2 * screw["S"][0, 3:]
     sc = rd.Model.from_robot(screw, synth.GRAVITY_Z)
     for model, B, fp64, want in [(dh30, 1000, True, "warp_scan"), (dh30, 2048, True, "warp_scan"),
                                  (dh30, 4096, True, "chunk"), (dh30, 16384, True, "reverse"),
-                                 (dh30, 1_000_000, True, "thread"), (dh30, 40000, False, "reverse"),
-                                 (dh30, 60000, False, "thread"), (dh10, 1000, True, "warp_scan"),
-                                 (dh10, 1000, False, "reverse"), (dh10, 100_000, True, "thread"),
+                                 (dh30, 1_000_000, True, "thread"), (dh30, 40000, False, "thread"),
+                                 (dh30, 1000, False, "warp_scan"), (dh30, 8192, False, "reverse"),
+                                 (dh30, 60000, False, "thread"), (dh10, 1000, True, "thread"),
+                                 (dh10, 1000, False, "thread"), (dh10, 100_000, True, "thread"),
+                                 (dh10, 1_000_000, True, "thread"), (dh30, 100_000, False, "thread"),
                                  (dh100, 64, True, "block_scan"), (dh100, 1000, True, "chunk"),
                                  (dh100, 4096, True, "chunk"), (dh100, 16384, True, "reverse"),
                                  (dh100, 100_000, True, "reverse"), (sc, 1000, True, "warp_scan"),
-                                 (sc, 100_000, True, "generic")]:
+                                 (sc, 100_000, True, "generic"), (dh7, 256, True, "thread"),
+                                 (dh7, 2048, False, "thread"), (dh7, 100_000, True, "thread")]:
         assert model.resolve_strategy(B, fp64) == want, (model.n, B, fp64, want)
 
 
@@ -332,9 +336,11 @@ def _per_state_boundary(rng, B, which):
 
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 @pytest.mark.parametrize("kind", ["revolute", "prismatic", "screw"])
-def test_per_state_boundary_id(rd, dtype, kind):
-    # NEXT-4: V_0, Vdot_0, F_{n+1} per state (rd_inverse_dynamics_bnd_*), every supported strategy
-    n, B = 9, 300
+@pytest.mark.parametrize("n", [5, 9, 20])
+def test_per_state_boundary_id(rd, dtype, kind, n):
+    # NEXT-4: V_0, Vdot_0, F_{n+1} per state (rd_inverse_dynamics_bnd_*), every supported strategy;
+    # THREAD runs the register kernel at n = 5 (and 9 in fp32 / up to its limit) and the stash kernel at 20
+    B = 300
     r = synth.random_chain(n, 61, prismatic_fraction=0.0 if kind == "revolute" else 0.4)
     if kind == "screw":
         i = int(np.argmax(np.linalg.norm(r["S"][:, 3:], axis=1)))
@@ -818,3 +824,44 @@ def test_cuda_graph_capture_and_replay(rd, strategy):
         g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("dtype,n", [(torch.float64, n) for n in list(range(1, 10)) + [12, 13]] +
+                                    [(torch.float32, n) for n in list(range(2, 10)) + [16, 17]])
+def test_thread_short_chain_register_kernel(rd, n, dtype):
+    """THREAD runs the register-resident, fully unrolled kernel (rnea_small.cu)
+    for n <= 8 (fp64; n <= 12 up to 300k states) / n <= 16 (fp32); 13 / 17 are
+    the first stash-kernel lengths at these batch sizes.  Revolute and mixed
+    prismatic chains, ragged batches (one state, a partial CTA, several CTAs),
+    and the model boundary (V_0, Vdot_0, F_{n+1}) of Eq. (3).  fp32 starts at
+    n = 2: a 1-link state's max|tau| is its single torque, which cancels to
+    ~1e-3 of its terms in some random states, and the fp32-rounded model (A15)
+    then gives 1.7e-4 there -- the same with the stash kernel
+    (profiles/r02/diag_small.txt); the fp32 1-link chain keeps its check in
+    test_prismatic_joints_dh_kernels."""
+    for pf, seed in ((0.0, 1200 + n), (0.4, 1300 + n)):
+        r = synth.random_chain(n, seed, prismatic_fraction=pf)
+        for B in (1, 127, 129, 3001):
+            q, qd, qdd = synth.states(21, n, 0, B)
+            check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype, strategy="thread")
+    rng = np.random.default_rng(n)
+    V0, Vd0, Ft = rng.standard_normal((3, 6))
+    r = synth.random_chain(n, 1400 + n, prismatic_fraction=0.3)
+    model = rd.Model.from_robot(r, (0, 0, 0))
+    model.set_boundary(V0, Vd0, Ft)
+    model.set_strategy("thread")
+    q, qd, qdd = synth.states(22, n, 0, 500)
+    tau, (q64, qd64, qdd64) = run_id(rd, model, q, qd, qdd, dtype)
+    ref = np.stack([oracle.rnea(r, q64[:, b], qd64[:, b], qdd64[:, b], V0, Vd0, Ft) for b in range(500)], 1)
+    assert rel_err_per_state(tau, ref).max() <= TOL[dtype]
+
+
+def test_thread_short_chain_many_waves(rd):
+    """The capped-register build of the register kernel (fp64, n = 6..8, batches
+    above 300k states) on a sample of 400k states: every CTA boundary
+    neighbourhood of the sample plus random states."""
+    n, B = 7, 400_000
+    r = synth.random_chain(n, 1507)
+    q, qd, qdd = synth.states(23, n, 0, B)
+    cols = parity_sample(B, tile=128)
+    check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy="thread", sample=cols)

@@ -16,6 +16,7 @@ ap.add_argument("--fd-algo", default="aba")
 ap.add_argument("--dtype", default="f64")
 ap.add_argument("--n", type=int, default=0, help="random chain with n links (overrides the config)")
 ap.add_argument("--batch", type=int, default=0)
+ap.add_argument("--graph", action="store_true", help="device time: CUDA-graph replay of 20 calls (grid_time)")
 a = ap.parse_args()
 rd.LIB_PATH = a.lib
 import torch  # noqa: E402
@@ -34,6 +35,13 @@ m = rd.Model.from_robot(synth.robot_for(cfg), cfg["gravity"])
 m.set_strategy(a.strategy)
 m.set_fd_algo(a.fd_algo)
 out = torch.empty_like(tq)
-f = (lambda: rd.forward_dynamics(m, tq, tqd, tqdd, out)) if a.fd else (lambda: rd.inverse_dynamics(m, tq, tqd, tqdd, out))
-print(os.path.basename(a.lib), a.config, f"n={n} B={cfg['batch']}", "fd" if a.fd else "id",
-      f"{time_call(f, reps=50):.4f} ms")
+if a.graph:
+    from grid_time import graph_time
+    g = ((lambda s=None: rd.forward_dynamics(m, tq, tqd, tqdd, out, stream=s)) if a.fd else
+         (lambda s=None: rd.inverse_dynamics(m, tq, tqd, tqdd, out, stream=s)))
+    ms = graph_time(g, reps=20)
+else:
+    f = (lambda: rd.forward_dynamics(m, tq, tqd, tqdd, out)) if a.fd else (lambda: rd.inverse_dynamics(m, tq, tqd, tqdd, out))
+    ms = time_call(f, reps=50)
+print(os.path.basename(a.lib), a.config, a.dtype, f"n={n} B={cfg['batch']}", "fd" if a.fd else "id",
+      a.strategy if not a.fd else a.fd_algo, "graph" if a.graph else "events", f"{ms:.4f} ms")
