@@ -54,8 +54,8 @@ typedef enum {
 typedef enum {
   RD_STRAT_AUTO = 0,      /* chosen per (n, dtype, batch) from the measured table */
   RD_STRAT_THREAD = 1,    /* one thread per state, serial recursion; revolute (zero pitch) and prismatic
-                             joints.  Short chains (fp64 n <= 8, or n <= 12 up to 300000 states; fp32
-                             n <= 32 except 25, 26) keep the whole per-link stash in registers (fully
+                             joints.  Short chains (fp64 n <= 12; fp32 n <= 32 except 25, 26) keep
+                             the whole per-link stash in registers (fully
                              unrolled register kernel); longer ones stash on chip (TMEM + shared memory),
                              n <= 30 fp64 / 32 fp32; otherwise falls back to REVERSE (screw: GENERIC) */
   RD_STRAT_WARP_SCAN = 2, /* one warp per state, lane = link, Kogge-Stone shuffle scans */

@@ -461,8 +461,8 @@ template <> const rd::Boundary<float>& bnd<float>(rd_model_t m) { return m->b32;
 // Strategy table, measured on B200 as device time
 // per call (CUDA-graph replay; profiles/r02/auto_grid_f64.csv, auto_grid_f32.csv).
 // DH chains (revolute / prismatic joints):
-//  * the register-resident THREAD kernel (rnea_small.cu; fp64 n <= 8 always, 9..12
-//    up to 300k states; fp32 n <= 32) except WARP_SCAN for the smallest batches of
+//  * the register-resident THREAD kernel (rnea_small.cu; fp64 n <= 12, fp32 n <= 32
+//    but 25, 26) except WARP_SCAN for the smallest batches of
 //    the longer chains and REVERSE for fp32 n >= 24 at 4-16k states (below);
 //  * n <= 32: WARP_SCAN (warp per state, lane = link; the latency regime of the
 //    paper) for batch <= 1536 (fp64: n >= 7; fp32: n >= 20), e.g. n = 30,
@@ -505,8 +505,8 @@ Plan resolve_plan(rd_model_t m, int64_t batch, bool fp64) {
     default: break;
   }
   if (m->dh_ok) {
-    // the register-resident THREAD kernel (rnea_small.cu: fp64 n <= 8 at any batch,
-    // 9..12 up to 300k states; fp32 n <= 32) wherever it is not beaten
+    // the register-resident THREAD kernel (rnea_small.cu: fp64 n <= 12, fp32 n <= 32
+    // but 25, 26) wherever it is not beaten
     // (profiles/r02/small_grid{,2,3}_f{64,32}.csv): n = 7, B = 256: 3.0 us vs 5.7
     // WARP_SCAN / 5.8 REVERSE, B = 1e6: 89 vs 161 us REVERSE; fp32 n = 30, 1e6: 0.218
     // vs 0.241 ms (stash kernel).  The warp scan keeps the smallest batches of the

@@ -106,7 +106,7 @@ cudaError_t launch_rnea_thread(int n, const LinkDHc<T>* L_host, const Boundary<T
                                int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
                                cudaStream_t st, int* launches, bool* supported, uint32_t prism_mask = 0,
                                const StateBoundary<T>* sb = nullptr);
-// Short chains (n <= 12 fp64 / 16 fp32, no per-state boundary): the register-resident, fully
+// Short chains (n <= 12 fp64 / 32 fp32): the register-resident, fully
 // unrolled THREAD kernel (rnea_small.cu); launch_rnea_thread dispatches to it.
 bool small_kernel_has_n(int n, bool fp64, int64_t batch);
 template <typename T>

@@ -11,12 +11,16 @@ namespace rd {
 #ifndef SMALL_MAX_F32
 #define SMALL_MAX_F32 32
 #endif
-// Longest chain per precision (the stash kernel takes longer ones).  fp64 chains
-// of 9..12 links spill (184-392 B uncapped): they win only below kSmallCapBatch
-// (n = 9, B = 1e5: 12.0 vs 19.1 us; 1e6: 147 vs 114 us, profiles/r02/ab_small_wide.txt).
+// Longest chain per precision (the stash kernel takes longer ones).  fp64 chains of
+// 9..12 links re-derive (sin, cos) in the backward sweep (small_recompute) and then
+// beat the stash kernel at every batch (n = 12, 1e6 states: 141.8 vs 148.7 us,
+// profiles/r02/ab_small_recompute_f64.csv); fp32 every n <= 32 but the spill cliff.
+#ifndef SMALL_MAX_F64
+#define SMALL_MAX_F64 12
+#endif
 template <typename T>
-constexpr int small_max_n() { return sizeof(T) == 8 ? 12 : SMALL_MAX_F32; }
-constexpr int kSmallMaxN64Any = 8;     // fp64: every batch size up to this n
+constexpr int small_max_n() { return sizeof(T) == 8 ? SMALL_MAX_F64 : SMALL_MAX_F32; }
+constexpr int kSmallMaxN64Any = SMALL_MAX_F64;   // fp64: every batch size up to this n
 // fp32 lengths where ptxas' allocation of the 255-register kernel falls off a
 // spill cliff (n = 25 / 26, 1e6 states: 317 / 367 us vs 191 us at n = 27;
 // profiles/r02/ab_small_f32_pack.csv): the stash kernel runs them.
@@ -27,7 +31,14 @@ constexpr int kSmallThreads = 128;
 // it spills ~150 B.  Measured (graph replay, n = 7): B = 1e5 8.8 us uncapped vs
 // 9.5 us capped; B = 1e6 96 vs 85 us -- the cap pays once there are many waves,
 // so both are built and the launch picks by batch (kSmallCapBatch).
-constexpr int64_t kSmallCapBatch = 300000;
+#ifndef SMALL_CAP_BATCH
+#define SMALL_CAP_BATCH 300000
+#endif
+#ifndef SMALL_CAP_MB
+#define SMALL_CAP_MB 3
+#endif
+constexpr int64_t kSmallCapBatch = SMALL_CAP_BATCH;
+constexpr int kSmallCapMB = SMALL_CAP_MB;      // resident CTAs per SM of the capped build
 template <typename T, int N>
 constexpr bool small_has_cap() { return sizeof(T) == 8 && N >= 6; }
 

@@ -41,6 +41,16 @@ struct SmallParams {
 // alignment costs more spills than the halved issue slots save (n = 30, 1e6:
 // 0.219 -> 0.304 ms; profiles/r02/ab_small_f32_pack.csv).
 __host__ __device__ constexpr bool small_f32_packed(int n) { return n == 7 || n == 8; }
+// Backward sweep re-deriving (sin, cos, d) of each link from q instead of keeping
+// them (two registers per link instead of six in fp64, for one more sincos per
+// link).  Measured (profiles/r02/ab_small_recompute*.csv, 1e6 states): fp64 n = 12
+// 66.4 -> 46.1 us at 262k states, 148.7 -> 141.8 us at 1e6 (the stash kernel:
+// 148.7); the capped build from n = 7 (n = 8: 104.6 -> 86.9 us); fp32 loses at
+// every n (n = 30: 0.220 -> 0.229 ms), its (sin, cos) cost one register each.
+template <typename T, int N, int MB>
+__host__ __device__ constexpr bool small_recompute() {
+  return sizeof(T) == 8 && (N >= 9 || (MB > 1 && N >= 7));
+}
 
 // fp32: the same recursion on packed pairs (rd_f32x2.cuh) -- (V_k, Vdot_k) through
 // the forward Ad, the ad term and the bias wrench, (f_k, m_k) through the backward
@@ -152,7 +162,7 @@ rnea_small_kernel(const __grid_constant__ SmallParams<T, N> P, int64_t B, const 
       Vdn[3] = fma(sr, Vn[4], Vdn[3]);
       Vdn[4] = fma(-sr, Vn[3], Vdn[4]);
       bias_force_com(C, Vn, Vdn, Fh[k]);
-      ss[k] = s; sc[k] = c; sd[k] = dl;
+      if constexpr (!small_recompute<T, N, MB>()) { ss[k] = s; sc[k] = c; sd[k] = dl; }
 #pragma unroll
       for (int j = 0; j < 6; ++j) { V[j] = Vn[j]; Vd[j] = Vdn[j]; }
     }
@@ -172,7 +182,18 @@ rnea_small_kernel(const __grid_constant__ SmallParams<T, N> P, int64_t B, const 
         for (int k = 0; k < 6; ++k) Fo[k] = Fh[i][k] + F[k];
       } else {
         const LinkDHc<T>& Cc = P.L[i + 1];
-        dh_bwd(Cc.ca, Cc.sa, Cc.a, sd[i + 1], ss[i + 1], sc[i + 1], F, Fh[i], Fo);
+        if constexpr (small_recompute<T, N, MB>()) {       // (sin, cos, d) of link i+1 again from q
+          const bool pc = PR && ((P.prism >> (i + 1)) & 1u);
+          T s1, c1, d1, qi = cq[i + 1];
+          // opaque copy: without it ptxas merges this sincos with the forward one and
+          // keeps (sin, cos) live across the sweeps again
+          if constexpr (sizeof(T) == 8) asm volatile("mov.b64 %0, %0;" : "+d"(qi));
+          else asm volatile("mov.b32 %0, %0;" : "+f"(qi));
+          dh_link<PR>(Cc, pc, qi, &s1, &c1, &d1);
+          dh_bwd(Cc.ca, Cc.sa, Cc.a, d1, s1, c1, F, Fh[i], Fo);
+        } else {
+          dh_bwd(Cc.ca, Cc.sa, Cc.a, sd[i + 1], ss[i + 1], sc[i + 1], F, Fh[i], Fo);
+        }
       }
 #pragma unroll
       for (int k = 0; k < 6; ++k) F[k] = Fo[k];
@@ -203,7 +224,7 @@ cudaError_t small_launch_n(const LinkDHc<T>* L_host, const Boundary<T>& bnd, int
   if (sb) {                                        // per-state boundary: uncapped build only
     launch_k<T, N, 1, true>(P, grid, B, q, qd, qdd, tau, st, *sb);
   } else if (small_has_cap<T, N>() && B > kSmallCapBatch) {
-    launch_k<T, N, small_has_cap<T, N>() ? 3 : 1, false>(P, grid, B, q, qd, qdd, tau, st, NoStateBoundary{});
+    launch_k<T, N, small_has_cap<T, N>() ? kSmallCapMB : 1, false>(P, grid, B, q, qd, qdd, tau, st, NoStateBoundary{});
   } else {
     launch_k<T, N, 1, false>(P, grid, B, q, qd, qdd, tau, st, NoStateBoundary{});
   }

@@ -827,11 +827,11 @@ def test_cuda_graph_capture_and_replay(rd, strategy):
 
 
 @pytest.mark.parametrize("dtype,n", [(torch.float64, n) for n in list(range(1, 10)) + [12, 13]] +
-                                    [(torch.float32, n) for n in list(range(2, 10)) + [16, 17]])
+                                    [(torch.float32, n) for n in list(range(2, 10)) + [16, 17, 25, 30]])
 def test_thread_short_chain_register_kernel(rd, n, dtype):
     """THREAD runs the register-resident, fully unrolled kernel (rnea_small.cu)
-    for n <= 8 (fp64; n <= 12 up to 300k states) / n <= 16 (fp32); 13 / 17 are
-    the first stash-kernel lengths at these batch sizes.  Revolute and mixed
+    for n <= 12 (fp64; the backward sweep re-derives sin/cos from n = 9) and
+    n <= 32 (fp32, but 25 and 26); 13 is the first fp64 stash-kernel length.  Revolute and mixed
     prismatic chains, ragged batches (one state, a partial CTA, several CTAs),
     and the model boundary (V_0, Vdot_0, F_{n+1}) of Eq. (3).  fp32 starts at
     n = 2: a 1-link state's max|tau| is its single torque, which cancels to
@@ -856,12 +856,13 @@ def test_thread_short_chain_register_kernel(rd, n, dtype):
     assert rel_err_per_state(tau, ref).max() <= TOL[dtype]
 
 
-def test_thread_short_chain_many_waves(rd):
-    """The capped-register build of the register kernel (fp64, n = 6..8, batches
-    above 300k states) on a sample of 400k states: every CTA boundary
-    neighbourhood of the sample plus random states."""
-    n, B = 7, 400_000
-    r = synth.random_chain(n, 1507)
+@pytest.mark.parametrize("n", [7, 12])
+def test_thread_short_chain_many_waves(rd, n):
+    """The capped-register build of the register kernel (fp64, n = 6..12, batches
+    above 300k states; n = 7 and 12 re-derive sin/cos in the backward sweep) on a
+    sample of 400k states: every CTA boundary neighbourhood plus random states."""
+    B = 400_000
+    r = synth.random_chain(n, 1500 + n, prismatic_fraction=0.3)
     q, qd, qdd = synth.states(23, n, 0, B)
     cols = parity_sample(B, tile=128)
     check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy="thread", sample=cols)

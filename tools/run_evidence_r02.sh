@@ -25,3 +25,6 @@ bash tools/run_ncu_one.sh aba_C4_f32 aba_dh --config C4 --fd --dtype f32 --reps 
 bash tools/run_ncu_one.sh rev_n100_1e6_f64 rnea_rev --config C4 --strategy reverse --batch 1000000 --reps 2 > /dev/null 2>&1
 for f in $R/bench_*.json; do echo "$f $(python -c "import json; d=json.loads(open('$f').read().strip().splitlines()[-1]); print(d.get('value'), d.get('ms_per_step'), (d.get('roofline') or {}).get('frac'))" 2>&1)"; done
 ls gpurun_out/ncu
+# keep gpurun_out/ under the 64 MiB copy-back limit: one full report, summaries + source pages for the rest
+for f in gpurun_out/ncu/*.ncu-rep; do [ "$(basename $f)" = "thread_C3_f64.ncu-rep" ] || rm -f $f; done
+du -sh gpurun_out
