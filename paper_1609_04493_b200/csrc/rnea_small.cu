@@ -10,8 +10,7 @@ namespace rd {
 bool small_kernel_has_n(int n, bool fp64, int64_t B) {
   if (n < 1) return false;
   if (!fp64) return n <= small_max_n<float>() && !small_f32_cliff(n);
-  (void)B;
-  return n <= kSmallMaxN64Any;
+  return n <= kSmallMaxN64Any || (n <= small_max_n<double>() && B <= kSmallCapBatch);
 }
 
 template <typename T, int N>

@@ -223,8 +223,9 @@ cudaError_t small_launch_n(const LinkDHc<T>* L_host, const Boundary<T>& bnd, int
   const int64_t grid = (B + kSmallThreads - 1) / kSmallThreads;
   if (sb) {                                        // per-state boundary: uncapped build only
     launch_k<T, N, 1, true>(P, grid, B, q, qd, qdd, tau, st, *sb);
-  } else if (small_has_cap<T, N>() && B > kSmallCapBatch) {
-    launch_k<T, N, small_has_cap<T, N>() ? kSmallCapMB : 1, false>(P, grid, B, q, qd, qdd, tau, st, NoStateBoundary{});
+  } else if (small_has_cap<T, N>() && B > small_cap_from<T, N>()) {
+    launch_k<T, N, small_has_cap<T, N>() ? small_cap_mb<T, N>() : 1, false>(P, grid, B, q, qd, qdd, tau, st,
+                                                                             NoStateBoundary{});
   } else {
     launch_k<T, N, 1, false>(P, grid, B, q, qd, qdd, tau, st, NoStateBoundary{});
   }

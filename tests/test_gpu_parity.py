@@ -826,12 +826,13 @@ def test_cuda_graph_capture_and_replay(rd, strategy):
     assert torch.equal(out, ref)
 
 
-@pytest.mark.parametrize("dtype,n", [(torch.float64, n) for n in list(range(1, 10)) + [12, 13]] +
+@pytest.mark.parametrize("dtype,n", [(torch.float64, n) for n in list(range(1, 10)) + [12, 13, 16, 17]] +
                                     [(torch.float32, n) for n in list(range(2, 10)) + [16, 17, 25, 30]])
 def test_thread_short_chain_register_kernel(rd, n, dtype):
     """THREAD runs the register-resident, fully unrolled kernel (rnea_small.cu)
-    for n <= 12 (fp64; the backward sweep re-derives sin/cos from n = 9) and
-    n <= 32 (fp32, but 25 and 26); 13 is the first fp64 stash-kernel length.  Revolute and mixed
+    for n <= 16 (fp64, 13..16 up to 300k states; the backward sweep re-derives
+    sin/cos from n = 9) and n <= 32 (fp32, but 25 and 26); 17 is the first fp64
+    stash-kernel length at these batch sizes.  Revolute and mixed
     prismatic chains, ragged batches (one state, a partial CTA, several CTAs),
     and the model boundary (V_0, Vdot_0, F_{n+1}) of Eq. (3).  fp32 starts at
     n = 2: a 1-link state's max|tau| is its single torque, which cancels to
