@@ -80,7 +80,9 @@ typedef enum {
 
 /* Forward-dynamics algorithm. */
 typedef enum {
-  RD_FD_ABA = 0,          /* articulated-body algorithm, Eq. (7)-(8), Alg. 3 (default) */
+  RD_FD_ABA = 0,          /* articulated-body algorithm, Eq. (7)-(8), Alg. 3 (default); one thread per
+                             state; revolute/prismatic chains of n <= 16 (fp64) / 20 (fp32) keep the per-link workspace in
+                             registers, longer ones in a per-call global workspace */
   RD_FD_JSIIA = 1,        /* joint-space inertia inversion, Eq. (6)/(17), Alg. 2: n+1 IDs per state
                              (one per lane of a warp, n <= 31, or per thread of a CTA, n <= 256) +
                              Cholesky solve; n > 256 -> RD_E_UNSUPPORTED */

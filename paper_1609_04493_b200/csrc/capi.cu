@@ -712,6 +712,12 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     if (e != cudaSuccess) return cuda_fail(e, "forward dynamics (scan ABIA) launch");
     return RD_OK;
   }
+  if (m->dh_ok && rd::aba_small_has_n(m->n, sizeof(T) == 8)) {   // short chain: workspace in registers
+    cudaError_t e = rd::launch_aba_small<T>(m->n, dh_consts<T>(m), dh_bnd<T>(m), batch, q, qd, tau, qdd, s,
+                                            &g_launches, status, m->prism_mask, usb ? &sbd : nullptr);
+    if (e != cudaSuccess) return cuda_fail(e, "forward dynamics (register ABA) launch");
+    return RD_OK;
+  }
   const int64_t slots = rd::generic_ws_slots(batch);
   st = ws_alloc(m, (size_t)slots * m->n * rd::aba_ws_per_link() * sizeof(T), s, &ws.p);
   if (st != RD_OK) return st;

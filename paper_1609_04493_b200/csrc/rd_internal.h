@@ -182,6 +182,13 @@ size_t jsiia_ws_elems(int n, int64_t B);   // workspace of the CTA-wide JSIIA (n
 int64_t generic_ws_slots(int64_t B);
 int generic_ws_per_link();
 int aba_ws_per_link();
+// Short chains (n <= 16 fp64 / 20 fp32, DH frames): ABA with the per-link workspace in registers
+// (aba_small.cuh); capi dispatches to it before launch_aba_dh.
+bool aba_small_has_n(int n, bool fp64);
+template <typename T>
+cudaError_t launch_aba_small(int n, const LinkDH<T>* L_host, const Boundary<T>& bnd, int64_t B, const T* q,
+                             const T* qd, const T* tau, T* qdd, cudaStream_t st, int* launches, int32_t* status,
+                             uint32_t prism_mask, const StateBoundary<T>* sb);
 
 bool thread_kernel_has_n(int n, bool fp64);
 int num_sms();

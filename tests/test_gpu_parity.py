@@ -867,3 +867,41 @@ def test_thread_short_chain_many_waves(rd, n):
     q, qd, qdd = synth.states(23, n, 0, B)
     cols = parity_sample(B, tile=128)
     check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy="thread", sample=cols)
+
+
+@pytest.mark.parametrize("dtype,n", [(torch.float64, n) for n in (1, 2, 3, 5, 7, 8, 9, 12, 16, 17)] +
+                                    [(torch.float32, n) for n in (2, 3, 5, 7, 8, 12, 20, 21)])
+def test_fd_short_chain_register_aba(rd, n, dtype):
+    """FD (ABA) for n <= 16 (fp64) / 20 (fp32) keeps sweep 2's per-link records
+    in registers (aba_small.cuh); 17 / 21 are the first workspace-kernel lengths.  Backward error
+    (A14) at the contract tolerance on revolute and mixed prismatic chains with
+    ragged batches, the per-state failing-pivot status, the model boundary and
+    per-state boundaries.  (fp32 from n = 2: a 1-link state's single torque can
+    cancel, reading A16.)"""
+    for pf, seed in ((0.0, 1600 + n), (0.4, 1700 + n)):
+        r = synth.random_chain(n, seed, prismatic_fraction=pf)
+        for B in (1, 129, 2000):
+            check_fd(rd, r, synth.GRAVITY_Z, B, 31, dtype, n_cond=8)
+    r = synth.random_chain(n, 1800 + n, prismatic_fraction=0.3)
+    model = rd.Model.from_robot(r, (0, 0, 0))
+    rng = np.random.default_rng(n)
+    V0, Vd0, Ft = rng.standard_normal((3, 6))
+    model.set_boundary(V0, Vd0, Ft)
+    B = 300
+    q, qd, qdd = (_rounded(x, dtype) for x in synth.states(32, n, 0, B))
+    tau = _rounded(np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b], V0, Vd0, Ft) for b in range(B)], 1), dtype)
+    st = torch.full((B,), -1, dtype=torch.int32, device="cuda")
+    out = rd.forward_dynamics(model, dev(q, dtype), dev(qd, dtype), dev(tau, dtype), status=st).double().cpu().numpy()
+    assert int(st.abs().max()) == 0
+    back = np.stack([oracle.rnea(r, q[:, b], qd[:, b], out[:, b], V0, Vd0, Ft) for b in range(B)], 1)
+    assert rel_err_per_state(back, tau).max() <= TOL[dtype]
+    # per-state boundary vectors (NEXT-4)
+    model2 = rd.Model.from_robot(r, synth.GRAVITY_Z)
+    Vs, Vds, Fs = (_rounded(a, dtype) for a in rng.standard_normal((3, 6, B)))
+    tau2 = _rounded(np.stack([oracle.rnea(r, q[:, b], qd[:, b], qdd[:, b], Vs[:, b], Vds[:, b], Fs[:, b])
+                              for b in range(B)], 1), dtype)
+    out2 = rd.forward_dynamics(model2, dev(q, dtype), dev(qd, dtype), dev(tau2, dtype),
+                               boundary=(dev(Vs, dtype), dev(Vds, dtype), dev(Fs, dtype))).double().cpu().numpy()
+    back2 = np.stack([oracle.rnea(r, q[:, b], qd[:, b], out2[:, b], Vs[:, b], Vds[:, b], Fs[:, b])
+                      for b in range(B)], 1)
+    assert rel_err_per_state(back2, tau2).max() <= TOL[dtype]
