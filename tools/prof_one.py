@@ -12,7 +12,10 @@ ap.add_argument("--dtype", default="f64")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--batch", type=int, default=0)
 ap.add_argument("--fd", action="store_true")
+ap.add_argument("--lib", default="")
 a = ap.parse_args()
+if a.lib:
+    rd.LIB_PATH = a.lib
 cfg = synth.CONFIGS[a.config]
 n = cfg["n"]; B = a.batch or cfg["batch"]
 dt = torch.float64 if a.dtype == "f64" else torch.float32
