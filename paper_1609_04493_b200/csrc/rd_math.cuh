@@ -12,6 +12,7 @@
 //   Ad^T_{f^-1}(f, m)     = (R f, p x (R f) + R m)
 #pragma once
 #include "rd_internal.h"
+#include "rd_f32x2.cuh"
 
 namespace rd {
 
@@ -347,14 +348,18 @@ __device__ __forceinline__ void dh_ad_f(const LinkDH<T>& C, T s, T c, const T* i
 
 // (sin, cos) of theta and the translation d of link C: revolute theta = th0 + q;
 // prismatic (PR && prism) theta = th0, d = d0 + q.
-template <bool PR, typename T, typename CT>
+// fp32: SC2 evaluates the sin and cos polynomials as one FFMA2 pair (sincos_f32x2,
+// bit-identical to rd_sincos(float)), opt-in where it measured faster (REVERSE fp32,
+// the register ID kernel up to n = 20; the register ABA lost 1.4-1.8x, ab_f32_sc2*).
+template <bool PR, bool SC2 = false, typename T, typename CT>
 __device__ __forceinline__ void dh_link(const CT& C, bool prism, T qi, T* s, T* c, T* d) {
   const T qa = (PR && prism) ? T(0) : qi;
-  if (sizeof(T) == 8) {
+  if constexpr (sizeof(T) == 8) {
     rd_sincos(qa + C.th0, s, c);
   } else {
     T s0, c0;
-    rd_sincos(qa, &s0, &c0);
+    if constexpr (SC2) sincos_f32x2(qa, &s0, &c0);
+    else rd_sincos(qa, &s0, &c0);
     *s = fma(s0, C.cth0, c0 * C.sth0);
     *c = fma(c0, C.cth0, -(s0 * C.sth0));
   }
