@@ -92,3 +92,37 @@ def test_oracle_and_product_share_no_code():
                 assert "oracle.cpp" not in txt and "liboracle" not in txt, f
     otxt = open(os.path.join(ROOT, "oracle", "oracle.cpp")).read()
     assert "rd_internal" not in otxt and "rd_math" not in otxt and "rd.h" not in otxt
+
+
+# ----------------------------------------------------------- the ABI from plain C
+def _build_c_example(rd, tmp_path):
+    """gcc the plain-C99 example (no CUDA headers, no Python) against include/rd.h and librd.so."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    exe = str(tmp_path / "planar2_c")
+    libdir = os.path.dirname(rd.LIB_PATH)
+    cmd = [cc, "-O2", "-std=c99", "-Wall", "-Wextra", "-Werror", f"-I{os.path.join(ROOT, 'include')}",
+           os.path.join(ROOT, "examples", "planar2_c.c"), f"-L{libdir}", "-lrd", f"-Wl,-rpath,{libdir}", "-lm",
+           "-o", exe]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_example_builds_against_the_header(rd, tmp_path):
+    # include/rd.h is plain C (C99, no torch / CUDA types) and librd.so links from C
+    _build_c_example(rd, tmp_path)
+
+
+@pytest.mark.gpu
+def test_c_example_runs(rd, tmp_path):
+    # examples/planar2_c.c: C1's robot through rd_model_create and the host-buffer ID / FD
+    # calls, checked in C against the textbook closed form and the FD round trip (1e-10)
+    import subprocess
+    exe = _build_c_example(rd, tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "planar2_c: ok" in r.stdout
