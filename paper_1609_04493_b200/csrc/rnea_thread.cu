@@ -24,6 +24,7 @@
 #include <type_traits>
 #include <cstdint>
 #include <cstdlib>
+#include <atomic>
 #include "rd_internal.h"
 #include "rd_math.cuh"
 #include "rd_f32x2.cuh"
@@ -530,12 +531,17 @@ rnea_thread_pp_kernel(const __grid_constant__ ThreadParams<T> P, int64_t B,
   if (warp == 0) tmem_dealloc_512(tmem_slot);
 }
 
+// SM count of the current device, cached per device ordinal (thread-safe).
 int num_sms() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  constexpr int kMaxDev = 64;
+  static std::atomic<int> cache[kMaxDev];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>* slot = (dev >= 0 && dev < kMaxDev) ? &cache[dev] : nullptr;
+  int sms = slot ? slot->load(std::memory_order_relaxed) : 0;
+  if (sms <= 0) {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    if (slot) slot->store(sms, std::memory_order_relaxed);
   }
   return sms;
 }
