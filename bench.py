@@ -340,16 +340,21 @@ def main():
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
         for k in range(args.steps):
-            if flush_buf is not None:
+            if flush_buf is not None:                  # flushed steps: events around each call
                 flush_buf.zero_()
-            evs[k][0].record(stream)
+                evs[k][0].record(stream)
             step()
-            evs[k][1].record(stream)
+            if flush_buf is not None:
+                evs[k][1].record(stream)
             launches += rd.last_launch_count()
         t_end.record(stream)
         torch.cuda.synchronize()
     barrier()
-    kernel_ms = [a.elapsed_time(b) for a, b in evs]
+    # inputs larger than L2: the K calls run back to back and the average launch duration
+    # is the bracketing events' span / K (per-call event pairs would add their own
+    # ~2-5 us record gaps to every step); flushed steps: the per-call event pairs
+    kernel_ms = ([a.elapsed_time(b) for a, b in evs] if flush_buf is not None
+                 else [t_start.elapsed_time(t_end) / args.steps])
     total_ms = t_start.elapsed_time(t_end) if flush_buf is None else sum(kernel_ms)
     avg_kernel_ms = float(np.mean(kernel_ms))
     total_ms, avg_kernel_ms = allreduce_max([total_ms, avg_kernel_ms])
