@@ -223,7 +223,7 @@ void rebuild_boundary(rd_model_t m) {
 
 // Modified-DH (Craig) frames for a chain of revolute (zero pitch) and prismatic
 // joints, from the joint frames (a prismatic joint slides along z_i: d = d0 + q):
-// G_i = pose of joint frame i in the base at q = 0 (z_i = joint axis).  Frame
+// joint frame i has z_i = the joint axis (Mp[i]: frame i in frame i-1).  Frame
 // D_i keeps z_i and puts its origin/x-axis on the common normal of axes i and
 // i+1 (any perpendicular for parallel axes; the joint frame itself for i = n);
 // D_0 := D_1, so f''_{0,1} = Rz(q_1).  Then D_{i-1}^-1 D_i = Rx(alpha) Tx(a)
@@ -231,25 +231,26 @@ void rebuild_boundary(rd_model_t m) {
 // (verified to 1e-10; otherwise the THREAD strategy is not used).
 bool build_dh(rd_model_t m, const std::vector<Rigid>& Mp, const std::vector<std::array<double, 36>>& Jp) {
   const int n = m->n;
-  std::vector<Rigid> G(n), D(n);
-  Rigid acc = rigid_identity();
-  for (int i = 0; i < n; ++i) { acc = rigid_mul(acc, Mp[i]); G[i] = acc; }
-  auto col = [](const Rigid& g, int c, double* v) { for (int k = 0; k < 3; ++k) v[k] = g.R[k][c]; };
+  // Every DH frame is built LOCALLY, as its pose D[i] in joint frame i from the axes
+  // of joints i and i+1 (joint frame i+1 in frame i is Mp[i+1]); then
+  // D_{i-1}^-1 D_i = D[i-1]^-1 Mp[i] D[i].  Building them from the base-frame poses
+  // G_i = Mp[0] ... Mp[i] instead carried the rounding of i products into every
+  // relative transform: ~1e-13 (n = 30) to ~1e-10 (n = 1000) relative torque error.
+  std::vector<Rigid> D(n);
   auto dot = [](const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; };
   auto cross = [](const double* a, const double* b, double* c) {
     c[0] = a[1] * b[2] - a[2] * b[1]; c[1] = a[2] * b[0] - a[0] * b[2]; c[2] = a[0] * b[1] - a[1] * b[0];
   };
   for (int i = 0; i < n; ++i) {
-    double z[3], o[3], x[3], P[3];
-    col(G[i], 2, z);
-    for (int k = 0; k < 3; ++k) o[k] = G[i].p[k];
+    const double z[3] = {0, 0, 1}, o[3] = {0, 0, 0};
+    double x[3], P[3];
     if (i == n - 1) {
-      col(G[i], 0, x);
+      x[0] = 1; x[1] = 0; x[2] = 0;
       for (int k = 0; k < 3; ++k) P[k] = o[k];
     } else {
-      double z2[3], o2[3], cz[3];
-      col(G[i + 1], 2, z2);
-      for (int k = 0; k < 3; ++k) o2[k] = G[i + 1].p[k];
+      const Rigid& N = Mp[i + 1];                       // joint frame i+1 in joint frame i
+      const double z2[3] = {N.R[0][2], N.R[1][2], N.R[2][2]}, o2[3] = {N.p[0], N.p[1], N.p[2]};
+      double cz[3];
       cross(z, z2, cz);
       const double cn = std::sqrt(dot(cz, cz));
       double w0[3] = {o[0] - o2[0], o[1] - o2[1], o[2] - o2[2]};
@@ -268,7 +269,7 @@ bool build_dh(rd_model_t m, const std::vector<Rigid>& Mp, const std::vector<std:
         for (int k = 0; k < 3; ++k) r[k] -= rz * z[k];
         const double rn = std::sqrt(dot(r, r));
         if (rn > 1e-12) for (int k = 0; k < 3; ++k) x[k] = r[k] / rn;
-        else col(G[i], 0, x);
+        else { x[0] = 1; x[1] = 0; x[2] = 0; }
         for (int k = 0; k < 3; ++k) P[k] = o[k];
       }
     }
@@ -279,13 +280,13 @@ bool build_dh(rd_model_t m, const std::vector<Rigid>& Mp, const std::vector<std:
       D[i].p[k] = P[k];
     }
   }
-  m->D0 = D[0];
+  m->D0 = rigid_mul(Mp[0], D[0]);                      // DH base frame in the user's base frame
   m->D64.resize(n);
   m->D32.resize(n);
   m->C64.resize(n);
   m->C32.resize(n);
   for (int i = 0; i < n; ++i) {
-    const Rigid Mi = (i == 0) ? rigid_identity() : rigid_mul(rigid_inv(D[i - 1]), D[i]);
+    const Rigid Mi = (i == 0) ? rigid_identity() : rigid_mul(rigid_inv(D[i - 1]), rigid_mul(Mp[i], D[i]));
     const double ca = Mi.R[2][2], sa = -Mi.R[1][2];
     const double ct = Mi.R[0][0], st = -Mi.R[0][1];
     const double a = Mi.p[0], d = -sa * Mi.p[1] + ca * Mi.p[2];
@@ -295,32 +296,53 @@ bool build_dh(rd_model_t m, const std::vector<Rigid>& Mp, const std::vector<std:
     for (int r = 0; r < 3; ++r)
       for (int c = 0; c < 3; ++c) err += std::fabs(Mi.R[r][c] - Rr[r][c]);
     if (!(err < 1e-10)) return false;
-    // inertia in the DH frame: E_i = G_i^-1 D_i (a rotation about / slide along z)
-    const Rigid E = rigid_mul(rigid_inv(G[i]), D[i]);
-    Mat6 A;
-    adjoint(E, A);
-    double Jd[6][6];
-    for (int r = 0; r < 6; ++r)
-      for (int c = 0; c < 6; ++c) {
+    // Inertia in the DH frame from the joint-frame inertia (the joint frame sits at the
+    // link, the DH origin can be metres away on the common normal): centre of mass
+    // c_j and rotational inertia I_c about it in the joint frame, then
+    // c = R_E^T (c_j - p_E), I_c' = R_E^T I_c R_E for E = G_i^-1 D_i, and the
+    // inertia about the DH origin I = I_c' + m (|c|^2 1 - c c^T).  (Congruence of
+    // the 6x6 J by Ad_E instead forms m |p_E|^2-sized terms and recovers I_c by
+    // cancellation: ~1e-11 relative torque error on long random chains.)
+    const Rigid& E = D[i];                                // DH frame i in joint frame i
+    const std::array<double, 36>& Jj = Jp[i];
+    const double mj = (Jj[0] + Jj[7] + Jj[14]) / 3.0;
+    const double hj[3] = {0.5 * (Jj[6 * 5 + 1] - Jj[6 * 4 + 2]), 0.5 * (Jj[6 * 3 + 2] - Jj[6 * 5 + 0]),
+                          0.5 * (Jj[6 * 4 + 0] - Jj[6 * 3 + 1])};
+    const double cj[3] = {hj[0] / mj, hj[1] / mj, hj[2] / mj};
+    double Icj[3][3];
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) Icj[r][c] = 0.5 * (Jj[6 * (3 + r) + 3 + c] + Jj[6 * (3 + c) + 3 + r]);
+    const double cj2 = cj[0] * cj[0] + cj[1] * cj[1] + cj[2] * cj[2];
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) Icj[r][c] -= mj * ((r == c ? cj2 : 0.0) - cj[r] * cj[c]);
+    double cd[3], Icd[3][3];
+    for (int r = 0; r < 3; ++r) {
+      double s = 0;
+      for (int k = 0; k < 3; ++k) s += E.R[k][r] * (cj[k] - E.p[k]);
+      cd[r] = s;
+    }
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) {
         double s = 0;
-        for (int k = 0; k < 6; ++k)
-          for (int l = 0; l < 6; ++l) s += A[k][r] * Jp[i][6 * k + l] * A[l][c];
-        Jd[r][c] = s;
+        for (int k = 0; k < 3; ++k)
+          for (int l = 0; l < 3; ++l) s += E.R[k][r] * Icj[k][l] * E.R[l][c];
+        Icd[r][c] = s;
       }
+    const double cd2 = cd[0] * cd[0] + cd[1] * cd[1] + cd[2] * cd[2];
     rd::LinkDH<double>& L = m->D64[i];
     L.ca = ca; L.sa = sa;
     L.a = a; L.d = d;
     L.th0 = std::atan2(st, ct);
     L.cth0 = std::cos(L.th0);
     L.sth0 = std::sin(L.th0);
-    L.m = (Jd[0][0] + Jd[1][1] + Jd[2][2]) / 3.0;
-    L.h[0] = 0.5 * (Jd[5][1] - Jd[4][2]);
-    L.h[1] = 0.5 * (Jd[3][2] - Jd[5][0]);
-    L.h[2] = 0.5 * (Jd[4][0] - Jd[3][1]);
-    L.I[0] = Jd[3][3]; L.I[1] = Jd[4][4]; L.I[2] = Jd[5][5];
-    L.I[3] = 0.5 * (Jd[3][4] + Jd[4][3]);
-    L.I[4] = 0.5 * (Jd[3][5] + Jd[5][3]);
-    L.I[5] = 0.5 * (Jd[4][5] + Jd[5][4]);
+    L.m = mj;
+    for (int k = 0; k < 3; ++k) L.h[k] = mj * cd[k];
+    L.I[0] = Icd[0][0] + mj * (cd2 - cd[0] * cd[0]);
+    L.I[1] = Icd[1][1] + mj * (cd2 - cd[1] * cd[1]);
+    L.I[2] = Icd[2][2] + mj * (cd2 - cd[2] * cd[2]);
+    L.I[3] = 0.5 * (Icd[0][1] + Icd[1][0]) - mj * cd[0] * cd[1];
+    L.I[4] = 0.5 * (Icd[0][2] + Icd[2][0]) - mj * cd[0] * cd[2];
+    L.I[5] = 0.5 * (Icd[1][2] + Icd[2][1]) - mj * cd[1] * cd[2];
     rd::LinkDH<float>& F = m->D32[i];
     F.ca = (float)L.ca; F.sa = (float)L.sa; F.a = (float)L.a; F.d = (float)L.d;
     F.th0 = (float)L.th0; F.m = (float)L.m;
@@ -331,14 +353,11 @@ bool build_dh(rd_model_t m, const std::vector<Rigid>& Mp, const std::vector<std:
     rd::LinkDHc<double>& Lc = m->C64[i];
     Lc.ca = L.ca; Lc.sa = L.sa; Lc.a = L.a; Lc.d = L.d;
     Lc.th0 = L.th0; Lc.cth0 = L.cth0; Lc.sth0 = L.sth0; Lc.m = L.m;
-    for (int k = 0; k < 3; ++k) Lc.c[k] = L.h[k] / L.m;
-    const double c2 = Lc.c[0] * Lc.c[0] + Lc.c[1] * Lc.c[1] + Lc.c[2] * Lc.c[2];
-    Lc.Ic[0] = L.I[0] - L.m * (c2 - Lc.c[0] * Lc.c[0]);
-    Lc.Ic[1] = L.I[1] - L.m * (c2 - Lc.c[1] * Lc.c[1]);
-    Lc.Ic[2] = L.I[2] - L.m * (c2 - Lc.c[2] * Lc.c[2]);
-    Lc.Ic[3] = L.I[3] + L.m * Lc.c[0] * Lc.c[1];
-    Lc.Ic[4] = L.I[4] + L.m * Lc.c[0] * Lc.c[2];
-    Lc.Ic[5] = L.I[5] + L.m * Lc.c[1] * Lc.c[2];
+    for (int k = 0; k < 3; ++k) Lc.c[k] = cd[k];                    // direct, no cancellation
+    Lc.Ic[0] = Icd[0][0]; Lc.Ic[1] = Icd[1][1]; Lc.Ic[2] = Icd[2][2];
+    Lc.Ic[3] = 0.5 * (Icd[0][1] + Icd[1][0]);
+    Lc.Ic[4] = 0.5 * (Icd[0][2] + Icd[2][0]);
+    Lc.Ic[5] = 0.5 * (Icd[1][2] + Icd[2][1]);
     rd::LinkDHc<float>& Fc = m->C32[i];
     Fc.ca = (float)Lc.ca; Fc.sa = (float)Lc.sa; Fc.a = (float)Lc.a; Fc.d = (float)Lc.d;
     Fc.th0 = (float)Lc.th0; Fc.cth0 = (float)Lc.cth0; Fc.sth0 = (float)Lc.sth0; Fc.m = (float)Lc.m;

@@ -803,6 +803,16 @@ def test_block_scan_long_chains(rd, n):
     check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, torch.float32, strategy="block_scan")
 
 
+@pytest.mark.parametrize("strategy", ["reverse", "generic", "chunk", "auto"])
+def test_very_long_chains(rd, strategy):
+    # n = 1000 (ten times the paper's longest ID chain): the strategies without a
+    # length cap; REVERSE re-derives V, Vdot through 1000 inverse maps (O(n eps) drift)
+    n = 1000
+    r = synth.random_chain(n, 1700, prismatic_fraction=0.05)
+    q, qd, qdd = synth.states(29, n, 0, 97)
+    check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strategy)
+
+
 @pytest.mark.parametrize("strategy", ["thread", "warp_scan", "generic", "reverse"])
 def test_cuda_graph_capture_and_replay(rd, strategy):
     # the launches are stream-ordered and host-synchronisation free, so a batch of
