@@ -803,6 +803,17 @@ def test_block_scan_long_chains(rd, n):
     check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, torch.float32, strategy="block_scan")
 
 
+@pytest.mark.parametrize("n, seed, tol", [(30, 1030, 2e-13), (100, 1800, 4e-12), (1000, 1700, 5e-12)])
+def test_dh_frames_built_locally(rd, n, seed, tol):
+    # Regression guard for the local DH construction: the DH-frame kernels
+    # (THREAD / REVERSE) agree with the oracle far inside the contract tolerance; building
+    # the frames from base-frame poses gave 6.5e-13 / 1.8e-11 / 2.5e-10 on these robots.
+    r = synth.random_chain(n, seed, prismatic_fraction=0.05)
+    q, qd, qdd = synth.states(29, n, 0, 97)
+    err = check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy="thread" if n <= 30 else "reverse")
+    assert err <= tol, f"DH-frame kernel error {err:.3e} > {tol:.0e}"
+
+
 @pytest.mark.parametrize("strategy", ["reverse", "generic", "chunk", "auto"])
 def test_very_long_chains(rd, strategy):
     # n = 1000 (ten times the paper's longest ID chain): the strategies without a
