@@ -280,6 +280,20 @@ bool build_dh(rd_model_t m, const std::vector<Rigid>& Mp, const std::vector<std:
       D[i].p[k] = P[k];
     }
   }
+  // Conditioning: nearly parallel consecutive axes put the common normal, and so the
+  // DH origin, far from the links; the DH maps then carry large, cancelling moment
+  // arms.  Measured (tools/near_parallel_accuracy.py, profiles/r02/near_parallel.csv):
+  // DH origin at 20 / 60 / 200 / 600 link lengths -> 5.6e-12 / 5.8e-11 / 7.5e-9 /
+  // 6.7e-8 relative torque error.  Beyond kDhMaxStretch the model keeps the
+  // joint-frame kernels only (exact to ~1e-14).
+  constexpr double kDhMaxStretch = 50.0;
+  double lref = 1e-9;
+  for (int i = 0; i < n; ++i)
+    lref = std::max(lref, std::sqrt(Mp[i].p[0] * Mp[i].p[0] + Mp[i].p[1] * Mp[i].p[1] + Mp[i].p[2] * Mp[i].p[2]));
+  for (int i = 0; i < n; ++i) {
+    const double off = std::sqrt(D[i].p[0] * D[i].p[0] + D[i].p[1] * D[i].p[1] + D[i].p[2] * D[i].p[2]);
+    if (!(off <= kDhMaxStretch * lref)) return false;
+  }
   m->D0 = rigid_mul(Mp[0], D[0]);                      // DH base frame in the user's base frame
   m->D64.resize(n);
   m->D32.resize(n);

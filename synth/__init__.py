@@ -172,6 +172,27 @@ def _rotx(a):
     return T
 
 
+def _roty(a):
+    T = np.eye(4)
+    c, s = np.cos(a), np.sin(a)
+    T[0, 0], T[0, 2], T[2, 0], T[2, 2] = c, s, -s, c
+    return T
+
+
+def tilted_planar(n: int, eps: float, seed: int):
+    """A planar n-link arm (all joint axes parallel to z) whose every joint axis is
+    tilted by ~eps rad (a calibrated, nominally planar arm): consecutive axes are
+    NEARLY parallel, so their common normal lies ~offset/eps away from the links."""
+    rng = np.random.default_rng(seed)
+    M, S, J = [], [], []
+    for i in range(n):
+        tilt = _rotx(eps * rng.choice([-1, 1]) * (0.5 + rng.random())) @ _roty(eps * rng.standard_normal())
+        M.append((_trans(0.4 + 0.2 * rng.random(), 0, 0.05 * rng.standard_normal()) if i else np.eye(4)) @ tilt)
+        S.append([0, 0, 0, 0, 0, 1.0])
+        J.append(spatial_inertia(1.0 + rng.random(), (0.2, 0.01, 0.0), np.diag([0.01, 0.02, 0.02])))
+    return {"M": np.array(M), "S": np.array(S), "J": np.array(J)}
+
+
 def pendulum(m: float = 1.7, l: float = 0.8, Izz: float = 0.0):
     """Single revolute link about z, mass m at (l, 0, 0), gravity -y.
 

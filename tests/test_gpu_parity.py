@@ -814,6 +814,24 @@ def test_dh_frames_built_locally(rd, n, seed, tol):
     assert err <= tol, f"DH-frame kernel error {err:.3e} > {tol:.0e}"
 
 
+@pytest.mark.parametrize("eps", [3e-2, 1e-2, 3e-3, 1e-3, 1e-4])
+@pytest.mark.parametrize("n", [6, 30])
+def test_nearly_parallel_axes(rd, n, eps):
+    # A calibrated, nominally planar arm: consecutive joint axes tilted by ~eps rad.  The
+    # DH origins move ~offset/eps off the links; beyond 50 link lengths the model keeps
+    # to the joint-frame kernels (at 200-600 link lengths the DH maps
+    # lost 2e-9 .. 7e-8).  Every strategy must hold the contract tolerance.
+    r = synth.tilted_planar(n, eps, 5 + n)
+    q, qd, qdd = synth.states(37, n, 0, 256)
+    for strategy in ("auto", "thread", "reverse"):
+        check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strategy)
+    model = rd.Model.from_robot(r, synth.GRAVITY_Z)
+    tau = oracle.rnea_batch(r, synth.GRAVITY_Z, q, qd, qdd)
+    qdd_fd = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()
+    back = oracle.rnea_batch(r, synth.GRAVITY_Z, q, qd, qdd_fd)
+    assert rel_err_per_state(back, tau).max() <= 1e-10
+
+
 @pytest.mark.parametrize("strategy", ["reverse", "generic", "chunk", "auto"])
 def test_very_long_chains(rd, strategy):
     # n = 1000 (ten times the paper's longest ID chain): the strategies without a
