@@ -51,10 +51,17 @@ typedef enum {
 } rd_status_t;
 
 /* In-robot parallelisation strategy of the inverse-dynamics kernel (north_star (2)). */
+/* THREAD, REVERSE and CHUNK run in Denavit-Hartenberg frames built from the model at
+ * creation.  They apply to chains of revolute (zero pitch) and prismatic joints whose DH
+ * origins lie within 50 link lengths of their joints; a model with screw joints, or with
+ * nearly parallel consecutive axes (DH origin farther out: ill-conditioned DH maps,
+ * DESIGN.md 8.5), runs every strategy on the joint-frame kernels (GENERIC / WARP_SCAN /
+ * BLOCK_SCAN) instead. */
 typedef enum {
   RD_STRAT_AUTO = 0,      /* chosen per (n, dtype, batch) from the measured table */
   RD_STRAT_THREAD = 1,    /* one thread per state, serial recursion; revolute (zero pitch) and prismatic
-                             joints.  Short chains (fp64 n <= 12; fp32 n <= 32 except 25, 26) keep
+                             joints.  Short chains (fp64 n <= 12, <= 16 up to 300k states; fp32 n <= 32
+                             except 25, 26) keep
                              the whole per-link stash in registers (fully
                              unrolled register kernel); longer ones stash on chip (TMEM + shared memory),
                              n <= 30 fp64 / 32 fp32; otherwise falls back to REVERSE (screw: GENERIC) */
