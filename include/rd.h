@@ -55,8 +55,8 @@ typedef enum {
  * creation.  They apply to chains of revolute (zero pitch) and prismatic joints whose DH
  * origins lie within 50 link lengths of their joints; a model with screw joints, or with
  * nearly parallel consecutive axes (DH origin farther out: ill-conditioned DH maps,
- * DESIGN.md 8.5), runs every strategy on the joint-frame kernels (GENERIC / WARP_SCAN /
- * BLOCK_SCAN) instead. */
+ * DESIGN.md 8.5), runs on the joint-frame kernels instead: THREAD and REVERSE as the
+ * joint-frame REVERSE kernel (any joints), CHUNK as GENERIC. */
 typedef enum {
   RD_STRAT_AUTO = 0,      /* chosen per (n, dtype, batch) from the measured table */
   RD_STRAT_THREAD = 1,    /* one thread per state, serial recursion; revolute (zero pitch) and prismatic
@@ -64,11 +64,12 @@ typedef enum {
                              except 25, 26) keep
                              the whole per-link stash in registers (fully
                              unrolled register kernel); longer ones stash on chip (TMEM + shared memory),
-                             n <= 30 fp64 / 32 fp32; otherwise falls back to REVERSE (screw: GENERIC) */
+                             n <= 30 fp64 / 32 fp32; otherwise falls back to REVERSE */
   RD_STRAT_WARP_SCAN = 2, /* one warp per state, lane = link, Kogge-Stone shuffle scans */
   RD_STRAT_GENERIC = 3,   /* one thread per state, any n, any joints, stash in a global workspace */
-  RD_STRAT_REVERSE = 4,   /* one thread per state, any n (revolute / prismatic joints; screw: GENERIC),
-                             no stash: the backward sweep re-derives V, Vdot by inverting the forward maps */
+  RD_STRAT_REVERSE = 4,   /* one thread per state, any n, any joints (DH frames for revolute / prismatic
+                             chains, joint frames otherwise), no stash: the backward sweep re-derives
+                             V, Vdot by inverting the forward maps */
   RD_STRAT_BLOCK_SCAN = 5, /* one CTA per state, thread = link, CTA-wide scans: the single-robot latency
                               mode for long chains (n <= 512) */
   RD_STRAT_WARP_SCAN_EQ13 = 6, /* the paper's operators literally: warp per state, one Eq. (13) semigroup scan

@@ -524,11 +524,13 @@ Plan resolve_plan(rd_model_t m, int64_t batch, bool fp64) {
   const int n = m->n;
   const bool thread_ok = m->dh_ok && rd::thread_kernel_has_n(n, fp64);
   const bool warp_ok = n <= 32;
+  // REVERSE exists in DH frames and in joint frames (any joints; constants in shared memory)
+  const bool rev_ok = m->dh_ok || rd::rev_jf_has_n(n, fp64);
   switch (m->strategy) {
     case RD_STRAT_GENERIC: return {RD_STRAT_GENERIC, 0};
-    case RD_STRAT_THREAD: return {thread_ok ? RD_STRAT_THREAD : (m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC), 0};
+    case RD_STRAT_THREAD: return {thread_ok ? RD_STRAT_THREAD : (rev_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC), 0};
     case RD_STRAT_WARP_SCAN: return {warp_ok ? RD_STRAT_WARP_SCAN : RD_STRAT_GENERIC, 0};
-    case RD_STRAT_REVERSE: return {m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC, 0};
+    case RD_STRAT_REVERSE: return {rev_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC, 0};
     case RD_STRAT_BLOCK_SCAN: return {n <= 512 ? RD_STRAT_BLOCK_SCAN : RD_STRAT_GENERIC, 0};
     case RD_STRAT_WARP_SCAN_EQ13: return {warp_ok ? RD_STRAT_WARP_SCAN_EQ13 : RD_STRAT_GENERIC, 0};
     case RD_STRAT_WARP_SCAN_EQ15: return {warp_ok ? RD_STRAT_WARP_SCAN_EQ15 : RD_STRAT_GENERIC, 0};
@@ -566,8 +568,15 @@ Plan resolve_plan(rd_model_t m, int64_t batch, bool fp64) {
     if (batch <= 6144 && n <= 300) return {RD_STRAT_CHUNK, n >= 150 ? 8 : 4};
     return {RD_STRAT_REVERSE, 0};
   }
-  if (warp_ok && batch <= kWarpScanMaxBatch) return {RD_STRAT_WARP_SCAN, 0};
+  // joint frames (screw joints, or no well-conditioned DH form): warp scan for small
+  // batches, then the joint-frame REVERSE, which needs no workspace: 1.6-2.3x GENERIC
+  // from n = 30 (n = 30, 1e6: 0.744 vs 1.191 ms; n = 100, 4096: 0.052 vs 0.118 ms) and
+  // 2.5x the warp scan for short chains at 4096 states (n = 7: 7.1 vs 17.7 us); GENERIC
+  // keeps short chains at large batches (n = 7, 1e5: 21.7 vs 24.0 us)
+  // (profiles/r02/jf_time.csv)
+  if (warp_ok && batch <= (n >= 16 ? kWarpScanMaxBatch : 1024)) return {RD_STRAT_WARP_SCAN, 0};
   if (!warp_ok && n <= 512 && batch <= kBlockScanMaxBatch) return {RD_STRAT_BLOCK_SCAN, 0};
+  if (rev_ok && !(n <= 8 && batch > 32768)) return {RD_STRAT_REVERSE, 0};
   return {RD_STRAT_GENERIC, 0};
 }
 
@@ -630,7 +639,7 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     make_state_boundary<T>(m, *usb, true, &sbd);
     pj = &sbj;
     pd = &sbd;
-    if (strat == RD_STRAT_BLOCK_SCAN || strat == RD_STRAT_CHUNK) strat = m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
+    if (strat == RD_STRAT_BLOCK_SCAN || strat == RD_STRAT_CHUNK) strat = RD_STRAT_REVERSE;   // (GENERIC if no REVERSE fits)
     if (strat == RD_STRAT_WARP_SCAN_EQ13 || strat == RD_STRAT_WARP_SCAN_EQ15)
       return fail(RD_E_UNSUPPORTED, "per-state boundary data: strategies THREAD, WARP_SCAN, GENERIC, REVERSE only");
   }
@@ -639,7 +648,7 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     bool ok = false;
     e = rd::launch_rnea_thread<T>(m->n, dhc_consts<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok,
                                   m->prism_mask, pd);
-    if (!ok) strat = m->dh_ok ? RD_STRAT_REVERSE : RD_STRAT_GENERIC;
+    if (!ok) strat = RD_STRAT_REVERSE;                 // (GENERIC if no REVERSE fits)
   } else if (strat == RD_STRAT_WARP_SCAN) {
     bool ok = false;
     e = rd::launch_rnea_warp<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok,
@@ -671,8 +680,13 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
                                  m->has_prism ? m->dPrism : nullptr, reinterpret_cast<T*>(ws.p));
   }
   if (strat == RD_STRAT_REVERSE) {
-    e = rd::launch_rnea_rev<T>(m->n, dhc_dev<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches,
-                               m->has_prism ? m->dPrism : nullptr, pd);
+    if (m->dh_ok)
+      e = rd::launch_rnea_rev<T>(m->n, dhc_dev<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches,
+                                 m->has_prism ? m->dPrism : nullptr, pd);
+    else if (rd::rev_jf_has_n(m->n, sizeof(T) == 8))    // joint frames: screw joints / ill-conditioned DH
+      e = rd::launch_rnea_rev_jf<T>(m->n, dev_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, pj);
+    else
+      strat = RD_STRAT_GENERIC;
   }
   if (strat == RD_STRAT_GENERIC) {
     const int64_t slots = rd::generic_ws_slots(batch);

@@ -149,6 +149,13 @@ cudaError_t launch_rnea_rev(int n, const LinkDHc<T>* L_dev, const Boundary<T>& b
                             int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
                             cudaStream_t st, int* launches, const unsigned char* prism = nullptr,
                             const StateBoundary<T>* sb = nullptr);
+// REVERSE in joint frames (rnea_rev_jf.cu): any joints (screw included), any n whose
+// constants fit shared memory; for models without a (well-conditioned) DH form.
+bool rev_jf_has_n(int n, bool fp64);
+template <typename T>
+cudaError_t launch_rnea_rev_jf(int n, const LinkConst<T>* L_dev, const Boundary<T>& bnd, int64_t B, const T* q,
+                               const T* qd, const T* qdd, T* tau, cudaStream_t st, int* launches,
+                               const StateBoundary<T>* sb = nullptr);
 // CHUNK (rnea_chunk.cu): `lanes` in {2, 4, 8, 16, 32} lanes per state; ws: device
 // workspace of chunk_ws_elems(n, B, lanes) elements.
 template <typename T>

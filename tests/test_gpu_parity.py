@@ -193,7 +193,7 @@ def test_auto_strategy_table(rd):
                                  (dh100, 64, True, "block_scan"), (dh100, 1000, True, "chunk"),
                                  (dh100, 4096, True, "chunk"), (dh100, 16384, True, "reverse"),
                                  (dh100, 100_000, True, "reverse"), (sc, 1000, True, "warp_scan"),
-                                 (sc, 100_000, True, "generic"), (dh7, 256, True, "thread"),
+                                 (sc, 100_000, True, "reverse"), (sc, 4096, True, "reverse"), (dh7, 256, True, "thread"),
                                  (dh7, 2048, False, "thread"), (dh7, 100_000, True, "thread")]:
         assert model.resolve_strategy(B, fp64) == want, (model.n, B, fp64, want)
 
@@ -274,8 +274,8 @@ def test_prismatic_and_screw_joints_generic(rd, dtype):
             r["S"][i, :3] += 0.2 * r["S"][i, 3:]
             break
     q, qd, qdd = synth.states(12, 12, 0, 2000)
-    for strat in ("generic", "warp_scan", "warp_scan_eq13", "warp_scan_eq15"):
-        check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype, strategy=strat)
+    for strat in ("generic", "warp_scan", "warp_scan_eq13", "warp_scan_eq15", "reverse", "thread", "auto"):
+        check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype, strategy=strat)   # reverse / thread: joint-frame REVERSE
 
 
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
@@ -449,9 +449,13 @@ def test_host_path_multichunk_workspace_kernels(rd):
     r["S"][i, :3] += 0.2 * r["S"][i, 3:]                    # screw joint -> GENERIC / joint-frame ABA
     q, qd, qdd = synth.states(18, n, 0, B)
     model = rd.Model.from_robot(r, synth.GRAVITY_Z)
-    assert model.resolve_strategy(B, True) == "generic"
+    assert model.resolve_strategy(B, True) == "reverse"      # AUTO: joint-frame REVERSE (no workspace)
+    auto_tau = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd)).cpu().numpy()
+    np.testing.assert_array_equal(rd.inverse_dynamics_host(model, q, qd, qdd), auto_tau)
+    model.set_strategy("generic")                             # the per-call workspace path
     dev_tau = rd.inverse_dynamics(model, dev(q), dev(qd), dev(qdd)).cpu().numpy()
     np.testing.assert_array_equal(rd.inverse_dynamics_host(model, q, qd, qdd), dev_tau)
+    assert rel_err_per_state(auto_tau, dev_tau).max() <= 1e-10
     sub = np.arange(0, B, 997)
     for algo in ("aba", "jsiia", "aba_scan"):
         model.set_fd_algo(algo)
@@ -830,6 +834,27 @@ def test_nearly_parallel_axes(rd, n, eps):
     qdd_fd = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()
     back = oracle.rnea_batch(r, synth.GRAVITY_Z, q, qd, qdd_fd)
     assert rel_err_per_state(back, tau).max() <= 1e-10
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("n", [1, 7, 30, 100, 333])
+def test_reverse_joint_frames(rd, n, dtype):
+    # REVERSE in joint frames (rnea_rev_jf.cu): screw joints (pitch on every third revolute
+    # joint), prismatic joints, ragged batch, model and per-state boundary
+    r = synth.random_chain(n, 900 + n, prismatic_fraction=0.3)
+    for i in range(0, n, 3):
+        if np.linalg.norm(r["S"][i, 3:]) > 0.5:
+            r["S"][i, :3] += 0.15 * r["S"][i, 3:]
+    q, qd, qdd = synth.states(43, n, 0, 517)
+    check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype, strategy="reverse")
+    model = rd.Model.from_robot(r, synth.GRAVITY_Z)
+    model.set_strategy("reverse")
+    B = q.shape[1]
+    bnd = tuple(dev(np.random.default_rng(k).standard_normal((6, B)), dtype) for k in range(3))
+    tau = rd.inverse_dynamics(model, dev(q, dtype), dev(qd, dtype), dev(qdd, dtype), boundary=bnd).cpu().numpy()
+    model.set_strategy("generic")
+    ref = rd.inverse_dynamics(model, dev(q, dtype), dev(qd, dtype), dev(qdd, dtype), boundary=bnd).cpu().numpy()
+    assert rel_err_per_state(tau, ref).max() <= TOL[dtype]
 
 
 @pytest.mark.parametrize("strategy", ["reverse", "generic", "chunk", "auto"])
