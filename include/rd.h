@@ -55,8 +55,9 @@ typedef enum {
  * creation.  They apply to chains of revolute (zero pitch) and prismatic joints whose DH
  * origins lie within 50 link lengths of their joints; a model with screw joints, or with
  * nearly parallel consecutive axes (DH origin farther out: ill-conditioned DH maps,
- * DESIGN.md 8.5), runs on the joint-frame kernels instead: THREAD and REVERSE as the
- * joint-frame REVERSE kernel (any joints), CHUNK as GENERIC. */
+ * DESIGN.md 8.5), runs on the joint-frame kernels instead (any joints): THREAD as the
+ * joint-frame register kernel (fp64 n <= 8, fp32 n <= 12) or else REVERSE, REVERSE in
+ * joint frames, CHUNK as GENERIC. */
 typedef enum {
   RD_STRAT_AUTO = 0,      /* chosen per (n, dtype, batch) from the measured table */
   RD_STRAT_THREAD = 1,    /* one thread per state, serial recursion; revolute (zero pitch) and prismatic

@@ -469,6 +469,9 @@ rd_status_t check_io(rd_model_t m, int64_t batch, const T* a, const T* b, const 
   return RD_OK;
 }
 
+template <typename T> const rd::LinkConst<T>* jf_consts(rd_model_t m);     // host copies (kernel parameters)
+template <> const rd::LinkConst<double>* jf_consts<double>(rd_model_t m) { return m->L64.data(); }
+template <> const rd::LinkConst<float>* jf_consts<float>(rd_model_t m) { return m->L32.data(); }
 template <typename T> const rd::LinkConst<T>* dev_consts(rd_model_t m);
 template <> const rd::LinkConst<double>* dev_consts<double>(rd_model_t m) { return m->dL64; }
 template <> const rd::LinkConst<float>* dev_consts<float>(rd_model_t m) { return m->dL32; }
@@ -522,7 +525,8 @@ struct Plan {
 
 Plan resolve_plan(rd_model_t m, int64_t batch, bool fp64) {
   const int n = m->n;
-  const bool thread_ok = m->dh_ok && rd::thread_kernel_has_n(n, fp64);
+  // THREAD: the DH kernels, or the joint-frame register kernel for short chains
+  const bool thread_ok = m->dh_ok ? rd::thread_kernel_has_n(n, fp64) : rd::small_jf_has_n(n, fp64);
   const bool warp_ok = n <= 32;
   // REVERSE exists in DH frames and in joint frames (any joints; constants in shared memory)
   const bool rev_ok = m->dh_ok || rd::rev_jf_has_n(n, fp64);
@@ -574,6 +578,7 @@ Plan resolve_plan(rd_model_t m, int64_t batch, bool fp64) {
   // 2.5x the warp scan for short chains at 4096 states (n = 7: 7.1 vs 17.7 us); GENERIC
   // keeps short chains at large batches (n = 7, 1e5: 21.7 vs 24.0 us)
   // (profiles/r02/jf_time.csv)
+  if (thread_ok) return {RD_STRAT_THREAD, 0};                  // joint-frame register kernel (short chains)
   if (warp_ok && batch <= (n >= 16 ? kWarpScanMaxBatch : 1024)) return {RD_STRAT_WARP_SCAN, 0};
   if (!warp_ok && n <= 512 && batch <= kBlockScanMaxBatch) return {RD_STRAT_BLOCK_SCAN, 0};
   if (rev_ok && !(n <= 8 && batch > 32768)) return {RD_STRAT_REVERSE, 0};
@@ -646,8 +651,13 @@ rd_status_t inverse_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
   cudaError_t e = cudaSuccess;
   if (strat == RD_STRAT_THREAD) {
     bool ok = false;
-    e = rd::launch_rnea_thread<T>(m->n, dhc_consts<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, &ok,
-                                  m->prism_mask, pd);
+    if (m->dh_ok) {
+      e = rd::launch_rnea_thread<T>(m->n, dhc_consts<T>(m), dh_bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches,
+                                    &ok, m->prism_mask, pd);
+    } else if (rd::small_jf_has_n(m->n, sizeof(T) == 8)) {
+      e = rd::launch_rnea_small_jf<T>(m->n, jf_consts<T>(m), bnd<T>(m), batch, q, qd, qdd, tau, s, &g_launches, pj);
+      ok = true;
+    }
     if (!ok) strat = RD_STRAT_REVERSE;                 // (GENERIC if no REVERSE fits)
   } else if (strat == RD_STRAT_WARP_SCAN) {
     bool ok = false;

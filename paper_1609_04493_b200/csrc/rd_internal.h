@@ -149,6 +149,13 @@ cudaError_t launch_rnea_rev(int n, const LinkDHc<T>* L_dev, const Boundary<T>& b
                             int64_t B, const T* q, const T* qd, const T* qdd, T* tau,
                             cudaStream_t st, int* launches, const unsigned char* prism = nullptr,
                             const StateBoundary<T>* sb = nullptr);
+// The register-resident THREAD kernel in joint frames (rnea_small_jf.cu): any joints,
+// short chains (fp64 n <= 8, fp32 n <= 12), for models without a (well-conditioned) DH form.
+bool small_jf_has_n(int n, bool fp64);
+template <typename T>
+cudaError_t launch_rnea_small_jf(int n, const LinkConst<T>* L_host, const Boundary<T>& bnd, int64_t B, const T* q,
+                                 const T* qd, const T* qdd, T* tau, cudaStream_t st, int* launches,
+                                 const StateBoundary<T>* sb = nullptr);
 // REVERSE in joint frames (rnea_rev_jf.cu): any joints (screw included), any n whose
 // constants fit shared memory; for models without a (well-conditioned) DH form.
 bool rev_jf_has_n(int n, bool fp64);

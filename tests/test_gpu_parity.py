@@ -857,6 +857,28 @@ def test_reverse_joint_frames(rd, n, dtype):
     assert rel_err_per_state(tau, ref).max() <= TOL[dtype]
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_thread_joint_frames_register_kernel(rd, dtype):
+    # the register-resident THREAD kernel in joint frames (rnea_small_jf.cu): screw and
+    # prismatic joints, n = 1..8 (fp64) / 1..12 (fp32), ragged batch, per-state boundary
+    for n in range(1, 9 if dtype == torch.float64 else 13):
+        r = synth.random_chain(n, 950 + n, prismatic_fraction=0.3)
+        for i in range(0, n, 2):
+            if np.linalg.norm(r["S"][i, 3:]) > 0.5:
+                r["S"][i, :3] += 0.1 * r["S"][i, 3:]
+        q, qd, qdd = synth.states(47, n, 0, 389)
+        check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, dtype, strategy="thread")
+        model = rd.Model.from_robot(r, synth.GRAVITY_Z)
+        assert model.resolve_strategy(389, dtype == torch.float64) == "thread"
+        B = q.shape[1]
+        bnd = tuple(dev(np.random.default_rng(k + n).standard_normal((6, B)), dtype) for k in range(3))
+        model.set_strategy("thread")
+        tau = rd.inverse_dynamics(model, dev(q, dtype), dev(qd, dtype), dev(qdd, dtype), boundary=bnd).cpu().numpy()
+        model.set_strategy("generic")
+        ref = rd.inverse_dynamics(model, dev(q, dtype), dev(qd, dtype), dev(qdd, dtype), boundary=bnd).cpu().numpy()
+        assert rel_err_per_state(tau, ref).max() <= TOL[dtype], n
+
+
 @pytest.mark.parametrize("strategy", ["reverse", "generic", "chunk", "auto"])
 def test_very_long_chains(rd, strategy):
     # n = 1000 (ten times the paper's longest ID chain): the strategies without a

@@ -18,14 +18,14 @@ def screw_chain(n, seed):
 
 
 print("robot,n,B,dtype,strategy,ms,auto")
-for name, n, r in (("tilted", 30, synth.tilted_planar(30, 1e-3, 35)), ("screw", 30, screw_chain(30, 930)),
-                   ("screw", 100, screw_chain(100, 1000)), ("screw", 7, screw_chain(7, 907))):
+for name, n, r in (("tilted", 6, synth.tilted_planar(6, 1e-3, 11)), ("screw", 7, screw_chain(7, 907)),
+                   ("screw", 12, screw_chain(12, 912)), ("tilted", 30, synth.tilted_planar(30, 1e-3, 35))):
     m = rd.Model.from_robot(r, synth.GRAVITY_Z)
     for dt in (torch.float64, torch.float32):
         for B in (4096, 16384, 100000, 1000000):
             tq, tqd, tqdd = synth.states_device(3, n, 0, B, dtype=dt)
             out = torch.empty_like(tq)
-            for s in ("generic", "reverse", "warp_scan", "auto"):
+            for s in ("generic", "reverse", "warp_scan", "thread", "auto"):
                 if s == "warp_scan" and (n > 32 or B > 100000):
                     continue
                 m.set_strategy(s)
