@@ -775,6 +775,12 @@ rd_status_t forward_dynamics(rd_model_t m, int64_t batch, const T* q, const T* q
     if (e != cudaSuccess) return cuda_fail(e, "forward dynamics (register ABA) launch");
     return RD_OK;
   }
+  if (!m->dh_ok && rd::aba_small_jf_has_n(m->n, sizeof(T) == 8)) {   // same in joint frames (any joints)
+    cudaError_t e = rd::launch_aba_small_jf<T>(m->n, jf_consts<T>(m), bnd<T>(m), batch, q, qd, tau, qdd, s,
+                                               &g_launches, status, usb ? &sbj : nullptr);
+    if (e != cudaSuccess) return cuda_fail(e, "forward dynamics (joint-frame register ABA) launch");
+    return RD_OK;
+  }
   const int64_t slots = rd::generic_ws_slots(batch);
   st = ws_alloc(m, (size_t)slots * m->n * rd::aba_ws_per_link() * sizeof(T), s, &ws.p);
   if (st != RD_OK) return st;

@@ -204,6 +204,13 @@ cudaError_t launch_aba_small(int n, const LinkDH<T>* L_host, const Boundary<T>& 
                              const T* qd, const T* tau, T* qdd, cudaStream_t st, int* launches, int32_t* status,
                              uint32_t prism_mask, const StateBoundary<T>* sb);
 
+// The register ABA in joint frames (aba_small_jf.cu): any joints, fp64 n <= 8 / fp32 n <= 12.
+bool aba_small_jf_has_n(int n, bool fp64);
+template <typename T>
+cudaError_t launch_aba_small_jf(int n, const LinkConst<T>* L_host, const Boundary<T>& bnd, int64_t B, const T* q,
+                                const T* qd, const T* tau, T* qdd, cudaStream_t st, int* launches, int32_t* status,
+                                const StateBoundary<T>* sb);
+
 bool thread_kernel_has_n(int n, bool fp64);
 int num_sms();
 

@@ -879,6 +879,35 @@ def test_thread_joint_frames_register_kernel(rd, dtype):
         assert rel_err_per_state(tau, ref).max() <= TOL[dtype], n
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_fd_joint_frames_register_aba(rd, dtype):
+    # the register ABA in joint frames (aba_small_jf.cu): screw and prismatic joints,
+    # n = 1..8 (fp64) / 1..12 (fp32), backward error at the contract tolerance, the status
+    # array, and the per-state boundary (consistent with ID under the same boundary)
+    for n in range(1, 9 if dtype == torch.float64 else 13):
+        r = synth.random_chain(n, 960 + n, prismatic_fraction=0.3)
+        for i in range(0, n, 2):
+            if np.linalg.norm(r["S"][i, 3:]) > 0.5:
+                r["S"][i, :3] += 0.1 * r["S"][i, 3:]
+        q, qd, qdd = synth.states(53, n, 0, 301)
+        model = rd.Model.from_robot(r, synth.GRAVITY_Z)
+        tq, tqd, tqdd = dev(q, dtype), dev(qd, dtype), dev(qdd, dtype)
+        B = q.shape[1]
+        bnd = tuple(dev(0.3 * np.random.default_rng(k + n).standard_normal((6, B)), dtype) for k in range(3))
+        tau = rd.inverse_dynamics(model, tq, tqd, tqdd, boundary=bnd)
+        status = torch.empty(B, dtype=torch.int32, device="cuda")
+        out = rd.forward_dynamics(model, tq, tqd, tau, boundary=bnd, status=status)
+        assert int(status.abs().sum()) == 0
+        back = rd.inverse_dynamics(model, tq, tqd, out, boundary=bnd)      # round trip through ID
+        err = rel_err_per_state(back.double().cpu().numpy(), tau.double().cpu().numpy()).max()
+        assert err <= (1e-10 if dtype == torch.float64 else 1e-4), (n, err)
+        # without a boundary, against the oracle's RNEA (backward error, A14)
+        tau0 = oracle.rnea_batch(r, synth.GRAVITY_Z, *(x.double().cpu().numpy() for x in (tq, tqd, tqdd)))
+        out0 = rd.forward_dynamics(model, tq, tqd, dev(tau0, dtype)).double().cpu().numpy()
+        back0 = oracle.rnea_batch(r, synth.GRAVITY_Z, tq.double().cpu().numpy(), tqd.double().cpu().numpy(), out0)
+        assert rel_err_per_state(back0, tau0).max() <= (1e-10 if dtype == torch.float64 else 1e-4), n
+
+
 @pytest.mark.parametrize("strategy", ["reverse", "generic", "chunk", "auto"])
 def test_very_long_chains(rd, strategy):
     # n = 1000 (ten times the paper's longest ID chain): the strategies without a
