@@ -908,6 +908,22 @@ def test_fd_joint_frames_register_aba(rd, dtype):
         assert rel_err_per_state(back0, tau0).max() <= (1e-10 if dtype == torch.float64 else 1e-4), n
 
 
+@pytest.mark.parametrize("B", [1, 2, 33, 129])
+def test_joint_frame_kernels_tiny_batches(rd, B):
+    # the joint-frame kernels at batches below one CTA / one warp (screw chain: no DH form)
+    for n in (1, 5, 40):
+        r = synth.random_chain(n, 970 + n, prismatic_fraction=0.3)
+        r["S"][0, :3] += 0.1 * r["S"][0, 3:] if np.linalg.norm(r["S"][0, 3:]) > 0.5 else 0.0
+        q, qd, qdd = synth.states(59, n, 0, B)
+        for strategy in ("thread", "reverse"):
+            check_id(rd, r, synth.GRAVITY_Z, q, qd, qdd, strategy=strategy)
+        model = rd.Model.from_robot(r, synth.GRAVITY_Z)
+        tau = oracle.rnea_batch(r, synth.GRAVITY_Z, q, qd, qdd)
+        out = rd.forward_dynamics(model, dev(q), dev(qd), dev(tau)).cpu().numpy()
+        back = oracle.rnea_batch(r, synth.GRAVITY_Z, q, qd, out)
+        assert rel_err_per_state(back, tau).max() <= 1e-10, (n, B)
+
+
 @pytest.mark.parametrize("strategy", ["reverse", "generic", "chunk", "auto"])
 def test_very_long_chains(rd, strategy):
     # n = 1000 (ten times the paper's longest ID chain): the strategies without a
