@@ -348,17 +348,32 @@ __device__ __forceinline__ void dh_ad_f(const LinkDH<T>& C, T s, T c, const T* i
 
 // (sin, cos) of theta and the translation d of link C: revolute theta = th0 + q;
 // prismatic (PR && prism) theta = th0, d = d0 + q.
-// fp32: SC2 evaluates the sin and cos polynomials as one FFMA2 pair (sincos_f32x2,
-// bit-identical to rd_sincos(float)), opt-in where it measured faster (REVERSE fp32,
-// the register ID kernel up to n = 20; the register ABA lost 1.4-1.8x, ab_f32_sc2*).
-template <bool PR, bool SC2 = false, typename T, typename CT>
+// fp32: kSc32Pair evaluates the sin and cos polynomials as one FFMA2 pair (sincos_f32x2,
+// bit-identical to rd_sincos(float)), opt-in where it measured faster (REVERSE fp32;
+// the register ABA lost 1.4-1.8x, ab_f32_sc2*); kSc32Mufu: sincos_mufu.
+// fp32 sin/cos on the special-function unit: reduction to [-pi, pi] with 2 pi split in
+// two floats, then sin.approx / cos.approx (PTX: max abs error 2^-20.9 there, ~8x the
+// polynomial's; used where the fp32 error stays far inside 1e-4: the register ID
+// kernel, n <= 32: 4.8e-6 at n = 30; REVERSE's inverse recursion amplified it to
+// 5.5e-5 at n = 200, so REVERSE keeps the polynomial; profiles/r02/ab_f32_mufu.txt).
+__device__ __forceinline__ void sincos_mufu(float x, float* sp, float* cp) {
+  const float k = rintf(x * 0.159154943f);
+  float r = fmaf(-k, 6.28318548f, x);
+  r = fmaf(-k, -1.74845553e-7f, r);
+  *sp = __sinf(r);
+  *cp = __cosf(r);
+}
+// fp32 sin/cos evaluation of dh_link (fp64 always uses rd_sincos).
+enum SinCos32 { kSc32Poly = 0, kSc32Pair = 1, kSc32Mufu = 2 };
+template <bool PR, int SC = kSc32Poly, typename T, typename CT>
 __device__ __forceinline__ void dh_link(const CT& C, bool prism, T qi, T* s, T* c, T* d) {
   const T qa = (PR && prism) ? T(0) : qi;
   if constexpr (sizeof(T) == 8) {
     rd_sincos(qa + C.th0, s, c);
   } else {
     T s0, c0;
-    if constexpr (SC2) sincos_f32x2(qa, &s0, &c0);
+    if constexpr (SC == kSc32Mufu) sincos_mufu(qa, &s0, &c0);
+    else if constexpr (SC == kSc32Pair) sincos_f32x2(qa, &s0, &c0);
     else rd_sincos(qa, &s0, &c0);
     *s = fma(s0, C.cth0, c0 * C.sth0);
     *c = fma(c0, C.cth0, -(s0 * C.sth0));

@@ -71,7 +71,7 @@ rnea_rev_kernel(int n, const LinkDHc<T>* __restrict__ Lg, const Boundary<T> bnd,
       const LinkDHc<T> C = L[i];
       const bool pz = PR && PRs[i];
       T s, c, dl;
-      dh_link<PR, true>(C, pz, qi, &s, &c, &dl);   // fp32: paired sin/cos (n = 100, 1e6: 1.144 -> 1.083 ms)
+      dh_link<PR, kSc32Pair>(C, pz, qi, &s, &c, &dl);   // fp32: paired sin/cos (n = 100, 1e6: 1.144 -> 1.083 ms)
       T Vn[6], Vdn[6];
       dh_ad_finv(C.ca, C.sa, C.a, dl, s, c, V, Vn);
       dh_ad_finv(C.ca, C.sa, C.a, dl, s, c, Vd, Vdn);
@@ -120,7 +120,7 @@ rnea_rev_kernel(int n, const LinkDHc<T>* __restrict__ Lg, const Boundary<T> bnd,
       for (int k = 0; k < 6; ++k) F[k] = Fo[k];
       tp = pz ? F[2] : F[5];                        // tau_i = S_i^T F_i
       T s, c, dl;
-      dh_link<PR, true>(C, pz, qi, &s, &c, &dl);   // fp32: paired sin/cos (n = 100, 1e6: 1.144 -> 1.083 ms)
+      dh_link<PR, kSc32Pair>(C, pz, qi, &s, &c, &dl);   // fp32: paired sin/cos (n = 100, 1e6: 1.144 -> 1.083 ms)
       // V_{i-1}, Vdot_{i-1}
       const T sr = pz ? T(0) : qdi, sp = pz ? qdi : T(0), ar = pz ? T(0) : qai, ap = pz ? qai : T(0);
       T x[6], y[6];

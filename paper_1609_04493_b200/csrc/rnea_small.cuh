@@ -52,11 +52,11 @@ __host__ __device__ constexpr bool small_recompute() {
   return sizeof(T) == 8 && (N >= 9 || (MB > 1 && N >= 7));
 }
 
-// fp32 sin/cos polynomials as one FFMA2 pair (dh_link SC2) where that measured faster:
-// n <= 20 but 15 (1e6 states: n = 12 0.0748 -> 0.0695 ms, 19 0.164 -> 0.146); from
-// n = 21 ptxas' allocation of the pairs costs more than the issue slots save (n = 30
-// 0.218 -> 0.246 ms; profiles/r02/ab_small_f32_sc2.csv).
-__host__ __device__ constexpr bool small_f32_sc2(int n) { return n <= 20 && n != 15; }
+// fp32 sin/cos on the SFU (dh_link kSc32Mufu): the fp32 kernel is issue-bound and the
+// polynomial is ~20 instructions per link (1e6 states: n = 12 0.0696 -> 0.0663 ms, 20
+// 0.1376 -> 0.1198, 30 0.2186 -> 0.2103; fp32 error 1.5e-6 -> 4.8e-6 at n = 30, contract
+// 1e-4; profiles/r02/ab_f32_mufu.txt).  (Before: the polynomial pair kSc32Pair for n <= 20,
+// profiles/r02/ab_small_f32_sc2.csv.)
 
 // fp32: the same recursion on packed pairs (rd_f32x2.cuh) -- (V_k, Vdot_k) through
 // the forward Ad, the ad term and the bias wrench, (f_k, m_k) through the backward
@@ -153,7 +153,7 @@ rnea_small_kernel(const __grid_constant__ SmallParams<T, N> P, int64_t B, const 
       const LinkDHc<T>& C = P.L[k];
       const bool prism = PR && ((P.prism >> k) & 1u);
       T s, c, dl;
-      dh_link<PR, small_f32_sc2(N)>(C, prism, cq[k], &s, &c, &dl);
+      dh_link<PR, kSc32Mufu>(C, prism, cq[k], &s, &c, &dl);
       T Vn[6], Vdn[6];
       dh_ad_finv(C.ca, C.sa, C.a, dl, s, c, V, Vn);
       dh_ad_finv(C.ca, C.sa, C.a, dl, s, c, Vd, Vdn);
@@ -195,7 +195,7 @@ rnea_small_kernel(const __grid_constant__ SmallParams<T, N> P, int64_t B, const 
           // keeps (sin, cos) live across the sweeps again
           if constexpr (sizeof(T) == 8) asm volatile("mov.b64 %0, %0;" : "+d"(qi));
           else asm volatile("mov.b32 %0, %0;" : "+f"(qi));
-          dh_link<PR, small_f32_sc2(N)>(Cc, pc, qi, &s1, &c1, &d1);
+          dh_link<PR, kSc32Mufu>(Cc, pc, qi, &s1, &c1, &d1);
           dh_bwd(Cc.ca, Cc.sa, Cc.a, d1, s1, c1, F, Fh[i], Fo);
         } else {
           dh_bwd(Cc.ca, Cc.sa, Cc.a, sd[i + 1], ss[i + 1], sc[i + 1], F, Fh[i], Fo);
